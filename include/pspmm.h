@@ -1,0 +1,235 @@
+/*
+ * pspmm.h — C ABI of the B200-native ParamSpMM hot path (libpspmm.so).
+ *
+ * The operation is the paper's SpMM  A_{n x n} . B_{n x dim} = C_{n x dim}
+ * (arXiv 2605.15695) with A held in Parameterized CSR
+ * (PCSR) and computed by a parametric engine configured by
+ * <W, F, V, S> (Alg. 2).  The three-phase workflow of P:192
+ * maps onto the calls below:
+ *   phase 1  configuration prediction : pspmm_features_compute + pspmm_decide_config
+ *   phase 2  PCSR generation          : pspmm_pcsr_build
+ *   phase 3  SpMM computing           : pspmm_spmm_run
+ * plus the row-shard helpers of the multi-GPU path.
+ *
+ * Conventions (apply to every call):
+ *  - Every call returns pspmm_status (0 == PSPMM_OK); no C++ exception ever
+ *    crosses the ABI.  pspmm_last_error() returns a thread-local message for
+ *    the most recent failure on the calling thread.
+ *  - "d_" pointers are CUDA device pointers (global memory of the current
+ *    device); "h_" pointers are host pointers.  `stream` is a cudaStream_t
+ *    passed as void* (NULL = the legacy default stream).
+ *  - Sparse matrices at the boundary are canonical CSR:
+ *    int32 rowPtr[n+1] with rowPtr[0] = 0, rowPtr[n] = nnz, non-decreasing;
+ *    int32 colIdx[nnz] strictly increasing inside each row, 0 <= col < n;
+ *    fp32 val[nnz].  A is square.
+ *  - Dense matrices are fp32 row-major with a leading dimension (ld >= K).
+ *    B is n x K (ldb), C is n x K (ldc).  The 128-bit path needs K % 4 == 0,
+ *    ld % 4 == 0 and 16-byte aligned B and C; otherwise the same engine runs
+ *    a masked scalar variant (correct, slower).  There is no CPU fallback.
+ *  - Memory passed in is caller-owned; the library never frees it.  A PCSR
+ *    handle owns its own device arrays until pspmm_pcsr_destroy.
+ *  - Indices are int32: n, nnz and nnz_V must be < 2^31 (else
+ *    PSPMM_ERR_UNSUPPORTED).
+ */
+#ifndef PSPMM_H
+#define PSPMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PSPMM_OK = 0,
+  PSPMM_ERR_INVALID_ARG = 1,     /* null pointer, negative size, bad omega ... */
+  PSPMM_ERR_NOT_CANONICAL = 2,   /* CSR violates the preconditions above */
+  PSPMM_ERR_DIM_MISMATCH = 3,    /* K < 1 or ld < K */
+  PSPMM_ERR_CONFIG = 4,          /* config outside its domain */
+  PSPMM_ERR_CONFIG_MISMATCH = 5, /* cfg.V / cfg.S / cfg.omega differ from the handle's */
+  PSPMM_ERR_EMPTY = 6,           /* features / SG undefined because nnz == 0 */
+  PSPMM_ERR_UNSUPPORTED = 7,     /* sizes beyond int32 indexing, unsupported mode */
+  PSPMM_ERR_OOM = 8,             /* device allocation failed */
+  PSPMM_ERR_CUDA = 9             /* any other CUDA runtime error */
+} pspmm_status;
+
+/*
+ * <W, F, V, S> of P:173 plus the build-specific knobs.
+ *  W  warps per CTA: 1, 2, 4, 8 or 16.
+ *  F  thread-coarsening factor, in B200 units: the number of
+ *     128-bit (4 x fp32) accumulators a lane keeps per output row, i.e. a
+ *     row group covers 4.G.F columns of C per pass.  1 .. 8.
+ *  V  vector size of vectorized blocking: 1 or 2.
+ *  S  workload balancing flag: 0 or 1.
+ *  omega  warp width used by Eq. 3; 32 on the device.  Other
+ *     values are accepted (>= 1) so small traces can be reproduced.
+ *  sg_override  0 = Split Granularity from Eq. 3; > 0 forces SG (c-18).
+ *  G  lanes per row group (1, 2, 4, 8, 16, 32); 0 = derived from K and F
+ *     as the smallest power of two with 4.G.F >= K (capped at 32).
+ *  mode  0 = CUDA-core engine (the only mode implemented; 1 is reserved for
+ *     the dense-panel tensor-core path and returns PSPMM_ERR_UNSUPPORTED).
+ * For pspmm_pcsr_build only V, S, omega and sg_override matter.
+ */
+typedef struct {
+  int32_t W, F, V, S;
+  int32_t omega;
+  int32_t sg_override;
+  int32_t G;
+  int32_t mode;
+} pspmm_config;
+
+typedef struct pspmm_pcsr_s *pspmm_pcsr; /* opaque, immutable after build */
+
+/* PCSR sizes and the metrics of Eq. 2 / Eq. 4. */
+typedef struct {
+  int64_t n;          /* rows of A (and of B, C) */
+  int64_t num_panels; /* ceil(n / V) */
+  int64_t nnz;        /* nonzeros of A */
+  int64_t nnz_v;      /* nonzero vectors (len(colIdx)); len(val) = nnz_v * V */
+  int64_t num_chunks; /* S = 1: chunks = len(TRow) = len(rowPtr) - 1; S = 0: num_panels */
+  int64_t sg;         /* split granularity used (S = 1), else 0 */
+  int32_t V, S, omega, reserved;
+  double pr;          /* PR_V = 1 - nnz / (nnz_V V)   (Eq. 2); NaN when nnz_v == 0 */
+  double sr;          /* SR = (chunks + 1) / (panels + 1)  (Eq. 4, c-4a); 1 when S = 0 */
+} pspmm_pcsr_info;
+
+/* The 16 Table-3 features, readings c-19 .. c-22 of DESIGN.md §3. */
+typedef struct {
+  double n, n_hat, nnz, delta, d, d_hat, d_max, cv, cv_hat, sr1, sr2, rho, b, b_max, pr1, pr2;
+} pspmm_features;
+
+/* Human-readable name of a status code (static storage). */
+const char *pspmm_status_string(pspmm_status s);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *pspmm_last_error(void);
+
+/* Library version string, e.g. "pspmm 0.1 sm_100a". */
+const char *pspmm_version(void);
+
+/*
+ * (a1) CSR intake check on the device: the canonical-CSR preconditions
+ * listed above.  Synchronises `stream` once to read the verdict.
+ * Returns PSPMM_OK or PSPMM_ERR_NOT_CANONICAL (or INVALID_ARG / CUDA).
+ */
+pspmm_status pspmm_csr_validate(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                                const int32_t *d_colidx, void *stream);
+
+/* Same check for an n_rows x n_cols CSR (0 <= col < n_cols). */
+pspmm_status pspmm_csr_validate_rect(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                     const int32_t *d_rowptr, const int32_t *d_colidx,
+                                     void *stream);
+
+/*
+ * (a4, a5) PCSR generation: vectorized blocking of A into
+ * ceil(n/V) panels of V x 1 nonzero vectors (ascending column order,
+ * +0.0f padding), then, if S == 1, the nonzero-split
+ * balancing of Eq. 3 (each panel's run cut into max(1, ceil(L/SG)) chunks,
+ * rowPtr reassigned, TRow[c] = source panel).  The integer arrays and the
+ * copied values are bit-identical to the oracle's (oracle/oracle.c).
+ * Validates the CSR first (pspmm_csr_validate).  V in {1, 2}; S in {0, 1};
+ * omega >= 1; sg_override >= 0 (0 = Eq. 3).  nnz == 0 with S == 1 and
+ * sg_override == 0 returns PSPMM_ERR_EMPTY (SG undefined).
+ * Allocates the handle's device arrays; synchronises `stream` (sizes).
+ * On success *out holds a new handle; on failure *out is NULL.
+ */
+pspmm_status pspmm_pcsr_build(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                              const int32_t *d_colidx, const float *d_val, int32_t V,
+                              int32_t S, int32_t omega, int32_t sg_override, void *stream,
+                              pspmm_pcsr *out);
+
+/*
+ * Same as pspmm_pcsr_build for a rectangular n_rows x n_cols CSR (columns
+ * checked against n_cols).  Used for the row shards of the multi-GPU path,
+ * whose columns index the all-gathered B (pspmm_shard_extract).  B then has
+ * n_cols rows and C has n_rows rows.
+ */
+pspmm_status pspmm_pcsr_build_rect(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                   const int32_t *d_rowptr, const int32_t *d_colidx,
+                                   const float *d_val, int32_t V, int32_t S, int32_t omega,
+                                   int32_t sg_override, void *stream, pspmm_pcsr *out);
+
+/* Sizes and metrics of a handle. */
+pspmm_status pspmm_pcsr_get_info(pspmm_pcsr A, pspmm_pcsr_info *out);
+
+/*
+ * Copy the four PCSR arrays to host memory (for bit-exact checks).
+ * h_rowptr: num_chunks + 1 int32 (S = 1) or num_panels + 1 (S = 0);
+ * h_colidx: nnz_v int32; h_val: nnz_v * V fp32; h_trow: num_chunks int32
+ * (S = 1 only; may be NULL when S = 0).  Any pointer may be NULL to skip
+ * that array.  Synchronous.
+ */
+pspmm_status pspmm_pcsr_export(pspmm_pcsr A, int32_t *h_rowptr, int32_t *h_colidx,
+                               float *h_val, int32_t *h_trow);
+
+/* Release a handle and its device arrays (NULL is a no-op). */
+void pspmm_pcsr_destroy(pspmm_pcsr A);
+
+/*
+ * (a6, a7) C = A . B (beta = 0) with the computing engine of Alg. 2
+ * configured by cfg: every output row of C is overwritten.
+ * cfg.V / cfg.S / cfg.omega must equal the handle's (else
+ * PSPMM_ERR_CONFIG_MISMATCH).  Asynchronous on `stream`; allocates nothing,
+ * so it can be captured in a CUDA graph.  With S = 1 the rows of split
+ * panels are zeroed by a small pre-kernel and accumulated with vector
+ * atomics (the accumulation order is then non-deterministic, c-23).
+ * Any K >= 1.  nnz_v == 0 writes zeros.
+ */
+pspmm_status pspmm_spmm_run(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
+                            int64_t ldc, pspmm_config cfg, void *stream);
+
+/*
+ * End-to-end variant for host-resident B and C (bench.py "e2e"): copies
+ * h_B (n x K, ldb) into the caller's device staging buffer d_Bbuf (same
+ * layout), runs pspmm_spmm_run into d_Cbuf (ldc), copies d_Cbuf back into
+ * h_C, and synchronises `stream`.  h_B / h_C should be pinned for the
+ * copies to be asynchronous.
+ */
+pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, int32_t K,
+                                 float *h_C, int64_t ldc, pspmm_config cfg, float *d_Bbuf,
+                                 float *d_Cbuf, void *stream);
+
+/*
+ * (a2) Table 3 features of a CSR matrix on the device.  Degree
+ * and bandwidth statistics are exact integer reductions; SR_1, SR_2, PR_1,
+ * PR_2 use the PCSR counting kernels with the given omega.  Synchronises
+ * `stream`.  nnz == 0 -> PSPMM_ERR_EMPTY.
+ */
+pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                                    const int32_t *d_colidx, int32_t omega, void *stream,
+                                    pspmm_features *out);
+
+/*
+ * (a3) SpMM-decider stand-in: a pure host function of
+ * (features, K) returning a valid <W, F, V, S> (+ G) for K.  The model is a
+ * decision tree trained on this repo's own autotune sweep.
+ */
+pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K, pspmm_config *out);
+
+/*
+ * (e) nnz-balanced contiguous row partition for P ranks (host).
+ * bounds[g] = min{ r : rowptr[r] >= ceil(g nnz / P) } rounded up to a
+ * multiple of `align` (>= 1) and clamped to n; bounds[0] = 0, bounds[P] = n.
+ * bounds must hold P + 1 entries.
+ */
+pspmm_status pspmm_shard_plan(int64_t n, const int32_t *h_rowptr, int32_t P, int32_t align,
+                              int64_t *bounds);
+
+/*
+ * (e) Local CSR of rank r's row shard with columns remapped into the padded
+ * all-gather layout of B: col' = owner(col) * n_max + (col - bounds[owner]),
+ * n_max = max_g (bounds[g+1] - bounds[g]).  Host arrays; h_lrowptr holds
+ * (bounds[r+1] - bounds[r] + 1) entries, h_lcolidx / h_lval hold
+ * rowptr[bounds[r+1]] - rowptr[bounds[r]] entries.  Columns stay strictly
+ * increasing per row (the remap is monotone).  *n_max_out receives n_max.
+ */
+pspmm_status pspmm_shard_extract(int64_t n, const int32_t *h_rowptr, const int32_t *h_colidx,
+                                 const float *h_val, int32_t P, const int64_t *bounds,
+                                 int32_t r, int32_t *h_lrowptr, int32_t *h_lcolidx,
+                                 float *h_lval, int64_t *n_max_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSPMM_H */

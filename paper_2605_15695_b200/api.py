@@ -1,0 +1,335 @@
+"""Thin Python binding of libpspmm.so (include/pspmm.h) — argument
+marshalling only: every step of the hot path runs in the library's CUDA
+kernels.  Device arrays are torch CUDA tensors (PyTorch is used for device
+memory and streams only); host arrays are numpy.  If the native library is
+missing this module raises at import time — there is no fallback.
+
+The functions carry the C names (pspmm_pcsr_build, pspmm_spmm_run, ...);
+`Pcsr` and `spmm` are small conveniences on top of them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpspmm.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is not built; run `python -m paper_2605_15695_b200.build_ext` "
+        "(the CUDA library is the only implementation — there is no fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+STATUS = ("PSPMM_OK", "PSPMM_ERR_INVALID_ARG", "PSPMM_ERR_NOT_CANONICAL",
+          "PSPMM_ERR_DIM_MISMATCH", "PSPMM_ERR_CONFIG", "PSPMM_ERR_CONFIG_MISMATCH",
+          "PSPMM_ERR_EMPTY", "PSPMM_ERR_UNSUPPORTED", "PSPMM_ERR_OOM", "PSPMM_ERR_CUDA")
+for _i, _name in enumerate(STATUS):
+    globals()[_name] = _i
+
+
+class PspmmError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib.pspmm_last_error().decode()
+        name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+        super().__init__(f"{where}: {name}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    """pspmm_config: <W, F, V, S> + omega, sg_override, G, mode."""
+    _fields_ = [(n, ctypes.c_int32) for n in ("W", "F", "V", "S", "omega", "sg_override", "G",
+                                              "mode")]
+
+    def __init__(self, W=4, F=1, V=1, S=0, omega=32, sg_override=0, G=0, mode=0):
+        super().__init__(W, F, V, S, omega, sg_override, G, mode)
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+    def __repr__(self):
+        return "Config(" + ", ".join(f"{k}={v}" for k, v in self.as_dict().items()) + ")"
+
+
+FEATURE_NAMES = ("n", "n_hat", "nnz", "delta", "d", "d_hat", "d_max", "cv", "cv_hat", "sr1",
+                 "sr2", "rho", "b", "b_max", "pr1", "pr2")
+
+
+class Features(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in FEATURE_NAMES]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n in FEATURE_NAMES}
+
+
+class PcsrInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("n", "num_panels", "nnz", "nnz_v", "num_chunks",
+                                              "sg")] + \
+        [(n, ctypes.c_int32) for n in ("V", "S", "omega", "reserved")] + \
+        [("pr", ctypes.c_double), ("sr", ctypes.c_double)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}
+
+
+_P = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_st = ctypes.c_int
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("pspmm_status_string", ctypes.c_char_p, _st)
+_sig("pspmm_last_error", ctypes.c_char_p)
+_sig("pspmm_version", ctypes.c_char_p)
+_sig("pspmm_csr_validate", _st, _i64, _i64, _P, _P, _P)
+_sig("pspmm_csr_validate_rect", _st, _i64, _i64, _i64, _P, _P, _P)
+_sig("pspmm_pcsr_build", _st, _i64, _i64, _P, _P, _P, _i32, _i32, _i32, _i32, _P,
+     ctypes.POINTER(_P))
+_sig("pspmm_pcsr_build_rect", _st, _i64, _i64, _i64, _P, _P, _P, _i32, _i32, _i32, _i32, _P,
+     ctypes.POINTER(_P))
+_sig("pspmm_pcsr_get_info", _st, _P, ctypes.POINTER(PcsrInfo))
+_sig("pspmm_pcsr_export", _st, _P, _P, _P, _P, _P)
+_sig("pspmm_pcsr_destroy", None, _P)
+_sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
+_sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
+_sig("pspmm_features_compute", _st, _i64, _i64, _P, _P, _i32, _P, ctypes.POINTER(Features))
+_sig("pspmm_decide_config", _st, ctypes.POINTER(Features), _i32, ctypes.POINTER(Config))
+_sig("pspmm_shard_plan", _st, _i64, _P, _i32, _i32, _P)
+_sig("pspmm_shard_extract", _st, _i64, _P, _P, _P, _i32, _P, _i32, _P, _P, _P,
+     ctypes.POINTER(_i64))
+
+
+def _check(status, where):
+    if status != 0:
+        raise PspmmError(status, where)
+
+
+def version() -> str:
+    return _lib.pspmm_version().decode()
+
+
+# ---------------------------------------------------------------- marshalling
+def _torch():
+    import torch
+    return torch
+
+
+def _dev(t, dtype, what):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{what} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dense(t, what):
+    """Row-major fp32 CUDA matrix with unit column stride -> (ptr, ld)."""
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+        raise TypeError(f"{what} must be a float32 CUDA tensor")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{what} must be 2-D row-major (stride(1) == 1)")
+    return ctypes.c_void_p(t.data_ptr()), max(t.stride(0), t.shape[1])
+
+
+def _stream(stream):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _host(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a, a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ---------------------------------------------------------------- ABI calls
+def pspmm_csr_validate(n, nnz, rowptr, colidx, stream=None, n_cols=None):
+    st = _lib.pspmm_csr_validate_rect(n, n if n_cols is None else n_cols, nnz,
+                                      _dev(rowptr, _torch().int32, "rowptr"),
+                                      _dev(colidx, _torch().int32, "colidx"), _stream(stream))
+    _check(st, "pspmm_csr_validate")
+
+
+class Pcsr:
+    """Owner of a pspmm_pcsr handle (destroyed with the object)."""
+
+    def __init__(self, handle, n_rows, n_cols):
+        self.handle = handle
+        self.n_rows = n_rows
+        self.n_cols = n_cols
+        self.info = pspmm_pcsr_get_info(self)
+
+    @property
+    def V(self):
+        return self.info["V"]
+
+    @property
+    def S(self):
+        return self.info["S"]
+
+    def run(self, B, C, cfg: Config, stream=None):
+        pspmm_spmm_run(self, B, C, cfg, stream)
+        return C
+
+    def export(self):
+        return pspmm_pcsr_export(self)
+
+    def close(self):
+        if self.handle is not None:
+            _lib.pspmm_pcsr_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pspmm_pcsr_build(n, nnz, rowptr, colidx, val, V, S, omega=32, sg_override=0, stream=None,
+                     n_cols=None) -> Pcsr:
+    torch = _torch()
+    h = ctypes.c_void_p()
+    nc = n if n_cols is None else n_cols
+    st = _lib.pspmm_pcsr_build_rect(n, nc, nnz, _dev(rowptr, torch.int32, "rowptr"),
+                                    _dev(colidx, torch.int32, "colidx"),
+                                    _dev(val, torch.float32, "val"), V, S, omega, sg_override,
+                                    _stream(stream), ctypes.byref(h))
+    _check(st, "pspmm_pcsr_build")
+    return Pcsr(h, n, nc)
+
+
+def pspmm_pcsr_get_info(A: Pcsr) -> dict:
+    info = PcsrInfo()
+    _check(_lib.pspmm_pcsr_get_info(A.handle, ctypes.byref(info)), "pspmm_pcsr_get_info")
+    return info.as_dict()
+
+
+def pspmm_pcsr_export(A: Pcsr) -> dict:
+    i = A.info
+    rl = (i["num_chunks"] if i["S"] else i["num_panels"]) + 1
+    rowptr = np.empty(rl, np.int32)
+    colidx = np.empty(i["nnz_v"], np.int32)
+    val = np.empty(i["nnz_v"] * i["V"], np.float32)
+    trow = np.empty(i["num_chunks"] if i["S"] else 0, np.int32)
+    st = _lib.pspmm_pcsr_export(A.handle, rowptr.ctypes.data_as(_P), colidx.ctypes.data_as(_P),
+                                val.ctypes.data_as(_P), trow.ctypes.data_as(_P) if i["S"] else None)
+    _check(st, "pspmm_pcsr_export")
+    return {"rowPtr": rowptr, "colIdx": colidx, "val": val, "TRow": trow, **i}
+
+
+def pspmm_pcsr_destroy(A: Pcsr):
+    A.close()
+
+
+def pspmm_spmm_run(A: Pcsr, B, C, cfg: Config, stream=None, K=None):
+    b, ldb = _dense(B, "B")
+    c, ldc = _dense(C, "C")
+    K = B.shape[1] if K is None else K
+    if C.shape[1] < K or B.shape[0] < A.n_cols or C.shape[0] < A.n_rows:
+        raise ValueError("B / C shapes do not match the PCSR handle and K")
+    _check(_lib.pspmm_spmm_run(A.handle, b, ldb, K, c, ldc, cfg, _stream(stream)),
+           "pspmm_spmm_run")
+
+
+def pspmm_spmm_run_host(A: Pcsr, hB, hC, cfg: Config, dB, dC, stream=None):
+    """hB / hC: pinned host torch tensors (or numpy) n x K fp32; dB / dC: device staging."""
+    torch = _torch()
+
+    def hptr(t):
+        if isinstance(t, torch.Tensor):
+            assert t.device.type == "cpu" and t.dtype == torch.float32 and t.is_contiguous()
+            return ctypes.c_void_p(t.data_ptr()), t.shape[1]
+        assert t.dtype == np.float32 and t.flags.c_contiguous
+        return t.ctypes.data_as(_P), t.shape[1]
+
+    hb, K = hptr(hB)
+    hc, _ = hptr(hC)
+    db, ldb = _dense(dB, "dB")
+    dc, ldc = _dense(dC, "dC")
+    _check(_lib.pspmm_spmm_run_host(A.handle, hb, ldb, K, hc, ldc, cfg, db, dc, _stream(stream)),
+           "pspmm_spmm_run_host")
+
+
+def pspmm_features_compute(n, nnz, rowptr, colidx, omega=32, stream=None) -> dict:
+    torch = _torch()
+    f = Features()
+    st = _lib.pspmm_features_compute(n, nnz, _dev(rowptr, torch.int32, "rowptr"),
+                                     _dev(colidx, torch.int32, "colidx"), omega, _stream(stream),
+                                     ctypes.byref(f))
+    _check(st, "pspmm_features_compute")
+    return f.as_dict()
+
+
+def pspmm_decide_config(features: dict, K: int) -> Config:
+    f = Features(*[float(features[k]) for k in FEATURE_NAMES])
+    c = Config()
+    _check(_lib.pspmm_decide_config(ctypes.byref(f), K, ctypes.byref(c)), "pspmm_decide_config")
+    return c
+
+
+def pspmm_shard_plan(rowptr, P: int, align: int = 1) -> np.ndarray:
+    rp, p = _host(rowptr, np.int32)
+    bounds = np.zeros(P + 1, np.int64)
+    _check(_lib.pspmm_shard_plan(rp.shape[0] - 1, p, P, align, bounds.ctypes.data_as(_P)),
+           "pspmm_shard_plan")
+    return bounds
+
+
+def pspmm_shard_extract(rowptr, colidx, val, P: int, bounds, r: int):
+    rp, prp = _host(rowptr, np.int32)
+    ci, pci = _host(colidx, np.int32)
+    vl, pvl = _host(val, np.float32)
+    bd, pbd = _host(bounds, np.int64)
+    n = rp.shape[0] - 1
+    lo, hi = int(bd[r]), int(bd[r + 1])
+    cnt = int(rp[hi]) - int(rp[lo])
+    lrp = np.empty(hi - lo + 1, np.int32)
+    lci = np.empty(max(cnt, 1), np.int32)
+    lvl = np.empty(max(cnt, 1), np.float32)
+    nmax = ctypes.c_int64()
+    st = _lib.pspmm_shard_extract(n, prp, pci, pvl, P, pbd, r, lrp.ctypes.data_as(_P),
+                                  lci.ctypes.data_as(_P), lvl.ctypes.data_as(_P),
+                                  ctypes.byref(nmax))
+    _check(st, "pspmm_shard_extract")
+    return lrp, lci[:cnt], lvl[:cnt], int(nmax.value)
+
+
+# ---------------------------------------------------------------- convenience
+def auto_config(n, nnz, rowptr, colidx, K, stream=None) -> Config:
+    """Phase 1 of P:192: Table-3 features on the device, then the decider."""
+    f = pspmm_features_compute(n, nnz, rowptr, colidx, stream=stream)
+    return pspmm_decide_config(f, K)
+
+
+def spmm(rowptr, colidx, val, B, cfg: Config | None = None, stream=None, C=None):
+    """The three-phase workflow in one call: features -> decider ->
+    PCSR -> engine.  Returns (C, cfg, Pcsr) so the handle can be reused."""
+    torch = _torch()
+    n = rowptr.shape[0] - 1
+    nnz = colidx.shape[0]
+    K = B.shape[1]
+    if cfg is None:
+        f = pspmm_features_compute(n, nnz, rowptr, colidx, stream=stream)
+        cfg = pspmm_decide_config(f, K)
+    A = pspmm_pcsr_build(n, nnz, rowptr, colidx, val, cfg.V, cfg.S, cfg.omega, cfg.sg_override,
+                         stream)
+    if C is None:
+        C = torch.empty((n, K), dtype=torch.float32, device=B.device)
+    A.run(B, C, cfg, stream)
+    return C, cfg, A

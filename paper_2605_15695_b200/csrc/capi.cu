@@ -1,0 +1,172 @@
+// extern "C" entry points of libpspmm.so (declared in include/pspmm.h).
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+
+namespace pspmm {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+pspmm_status cuda_status(cudaError_t e, const char *where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();  // clear sticky-free errors
+  return e == cudaErrorMemoryAllocation ? PSPMM_ERR_OOM : PSPMM_ERR_CUDA;
+}
+
+}  // namespace pspmm
+
+using namespace pspmm;
+
+extern "C" {
+
+const char *pspmm_status_string(pspmm_status s) {
+  switch (s) {
+    case PSPMM_OK: return "PSPMM_OK";
+    case PSPMM_ERR_INVALID_ARG: return "PSPMM_ERR_INVALID_ARG";
+    case PSPMM_ERR_NOT_CANONICAL: return "PSPMM_ERR_NOT_CANONICAL";
+    case PSPMM_ERR_DIM_MISMATCH: return "PSPMM_ERR_DIM_MISMATCH";
+    case PSPMM_ERR_CONFIG: return "PSPMM_ERR_CONFIG";
+    case PSPMM_ERR_CONFIG_MISMATCH: return "PSPMM_ERR_CONFIG_MISMATCH";
+    case PSPMM_ERR_EMPTY: return "PSPMM_ERR_EMPTY";
+    case PSPMM_ERR_UNSUPPORTED: return "PSPMM_ERR_UNSUPPORTED";
+    case PSPMM_ERR_OOM: return "PSPMM_ERR_OOM";
+    case PSPMM_ERR_CUDA: return "PSPMM_ERR_CUDA";
+  }
+  return "PSPMM_UNKNOWN_STATUS";
+}
+
+const char *pspmm_last_error(void) { return g_last_error.c_str(); }
+
+const char *pspmm_version(void) { return "pspmm 0.1 sm_100a"; }
+
+pspmm_status pspmm_csr_validate_rect(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                     const int32_t *d_rowptr, const int32_t *d_colidx,
+                                     void *stream) {
+  return validate_csr(n_rows, n_cols, nnz, d_rowptr, d_colidx, as_stream(stream));
+}
+
+pspmm_status pspmm_csr_validate(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                                const int32_t *d_colidx, void *stream) {
+  return validate_csr(n, n, nnz, d_rowptr, d_colidx, as_stream(stream));
+}
+
+pspmm_status pspmm_pcsr_build_rect(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                   const int32_t *d_rowptr, const int32_t *d_colidx,
+                                   const float *d_val, int32_t V, int32_t S, int32_t omega,
+                                   int32_t sg_override, void *stream, pspmm_pcsr *out) {
+  if (!out) {
+    set_error("pcsr_build: null out");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  *out = nullptr;
+  pspmm_pcsr_s *A = new (std::nothrow) pspmm_pcsr_s();
+  if (!A) {
+    set_error("pcsr_build: host allocation failed");
+    return PSPMM_ERR_OOM;
+  }
+  pspmm_status st = build_pcsr(n_rows, n_cols, nnz, d_rowptr, d_colidx, d_val, V, S, omega,
+                               sg_override, as_stream(stream), A);
+  if (st != PSPMM_OK) {
+    pspmm_pcsr_destroy(A);
+    return st;
+  }
+  *out = A;
+  return PSPMM_OK;
+}
+
+pspmm_status pspmm_pcsr_build(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                              const int32_t *d_colidx, const float *d_val, int32_t V, int32_t S,
+                              int32_t omega, int32_t sg_override, void *stream, pspmm_pcsr *out) {
+  return pspmm_pcsr_build_rect(n, n, nnz, d_rowptr, d_colidx, d_val, V, S, omega, sg_override,
+                               stream, out);
+}
+
+pspmm_status pspmm_pcsr_get_info(pspmm_pcsr A, pspmm_pcsr_info *out) {
+  if (!A || !out) {
+    set_error("pcsr_get_info: null argument");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  std::memset(out, 0, sizeof(*out));
+  out->n = A->n_rows;
+  out->num_panels = A->num_panels;
+  out->nnz = A->nnz;
+  out->nnz_v = A->nnz_v;
+  out->num_chunks = A->num_chunks;
+  out->sg = A->sg;
+  out->V = A->V;
+  out->S = A->S;
+  out->omega = A->omega;
+  out->pr = A->pr;
+  out->sr = A->sr;
+  return PSPMM_OK;
+}
+
+pspmm_status pspmm_pcsr_export(pspmm_pcsr A, int32_t *h_rowptr, int32_t *h_colidx, float *h_val,
+                               int32_t *h_trow) {
+  if (!A) {
+    set_error("pcsr_export: null handle");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  if (h_rowptr)
+    PSPMM_CUDA_TRY(cudaMemcpy(h_rowptr, A->d_rowptr, (size_t)A->rowptr_len * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost));
+  if (h_colidx && A->nnz_v)
+    PSPMM_CUDA_TRY(cudaMemcpy(h_colidx, A->d_colidx, (size_t)A->nnz_v * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost));
+  if (h_val && A->nnz_v)
+    PSPMM_CUDA_TRY(cudaMemcpy(h_val, A->d_val, (size_t)A->nnz_v * A->V * sizeof(float),
+                              cudaMemcpyDeviceToHost));
+  if (h_trow && A->S == 1 && A->num_chunks)
+    PSPMM_CUDA_TRY(cudaMemcpy(h_trow, A->d_trow, (size_t)A->num_chunks * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost));
+  return PSPMM_OK;
+}
+
+void pspmm_pcsr_destroy(pspmm_pcsr A) {
+  if (!A) return;
+  cudaFree(A->d_rowptr);
+  cudaFree(A->d_colidx);
+  cudaFree(A->d_val);
+  cudaFree(A->d_trow);
+  cudaFree(A->d_split);
+  delete A;
+}
+
+pspmm_status pspmm_spmm_run(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
+                            int64_t ldc, pspmm_config cfg, void *stream) {
+  return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream));
+}
+
+pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, int32_t K,
+                                 float *h_C, int64_t ldc, pspmm_config cfg, float *d_Bbuf,
+                                 float *d_Cbuf, void *stream) {
+  if (!A || !h_B || !h_C || !d_Bbuf || !d_Cbuf) {
+    set_error("spmm_run_host: null argument");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  if (K < 1 || ldb < K || ldc < K) {
+    set_error("spmm_run_host: need K >= 1, ldb >= K, ldc >= K");
+    return PSPMM_ERR_DIM_MISMATCH;
+  }
+  cudaStream_t s = as_stream(stream);
+  PSPMM_CUDA_TRY(cudaMemcpyAsync(d_Bbuf, h_B, (size_t)A->n_cols * ldb * sizeof(float),
+                                 cudaMemcpyHostToDevice, s));
+  pspmm_status st = run_spmm(A, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, s);
+  if (st != PSPMM_OK) return st;
+  PSPMM_CUDA_TRY(cudaMemcpyAsync(h_C, d_Cbuf, (size_t)A->n_rows * ldc * sizeof(float),
+                                 cudaMemcpyDeviceToHost, s));
+  PSPMM_CUDA_TRY(cudaStreamSynchronize(s));
+  return PSPMM_OK;
+}
+
+pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                                    const int32_t *d_colidx, int32_t omega, void *stream,
+                                    pspmm_features *out) {
+  return compute_features(n, nnz, d_rowptr, d_colidx, omega, as_stream(stream), out);
+}
+
+}  // extern "C"

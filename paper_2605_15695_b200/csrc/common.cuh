@@ -1,0 +1,79 @@
+// Internal declarations of libpspmm.so (not part of the ABI; see include/pspmm.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "pspmm.h"
+
+// The PCSR handle: rowPtr / colIdx / val / TRow on the device, plus
+// derived data that is NOT part of the bit-exact PCSR contract:
+//   d_split  = ids of panels that own more than one chunk (S = 1); their C
+//              rows are zeroed before the chunks accumulate into them.
+struct pspmm_pcsr_s {
+  int64_t n_rows = 0, n_cols = 0, num_panels = 0, nnz = 0, nnz_v = 0, num_chunks = 0;
+  int64_t sg = 0, rowptr_len = 0, num_split = 0;
+  int32_t V = 1, S = 0, omega = 32;
+  double pr = 0.0, sr = 1.0;
+  int32_t *d_rowptr = nullptr;  // rowptr_len
+  int32_t *d_colidx = nullptr;  // nnz_v
+  float *d_val = nullptr;       // nnz_v * V
+  int32_t *d_trow = nullptr;    // num_chunks (S = 1)
+  int32_t *d_split = nullptr;   // num_split (S = 1)
+};
+
+namespace pspmm {
+
+void set_error(const std::string &msg);
+pspmm_status cuda_status(cudaError_t e, const char *where);
+
+#define PSPMM_CUDA_TRY(expr)                                      \
+  do {                                                            \
+    cudaError_t _e = (expr);                                      \
+    if (_e != cudaSuccess) return ::pspmm::cuda_status(_e, #expr); \
+  } while (0)
+
+#define PSPMM_FAIL(code, msg)          \
+  do {                                 \
+    ::pspmm::set_error(msg);           \
+    return code;                       \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// validate.cu
+pspmm_status validate_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t *d_rowptr,
+                          const int32_t *d_colidx, cudaStream_t stream);
+
+// pcsr_build.cu
+pspmm_status build_pcsr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t *d_rowptr,
+                        const int32_t *d_colidx, const float *d_val, int32_t V, int32_t S,
+                        int32_t omega, int32_t sg_override, cudaStream_t stream,
+                        pspmm_pcsr_s *P);
+// per-panel vector counts |union_p| for V = 2 (shared with features.cu)
+pspmm_status panel_counts_v2(int64_t n_rows, const int32_t *d_rowptr, const int32_t *d_colidx,
+                             int32_t *d_L, cudaStream_t stream);
+
+// spmm.cu
+pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
+                      int64_t ldc, const pspmm_config &cfg, cudaStream_t stream);
+
+// features.cu
+pspmm_status compute_features(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                              const int32_t *d_colidx, int32_t omega, cudaStream_t stream,
+                              pspmm_features *out);
+
+}  // namespace pspmm

@@ -1,0 +1,87 @@
+// (a3) SpMM-decider stand-in (§5.2): a pure host
+// function of (Table-3 features, K) -> <W, F, V, S> (+ G).  The paper uses a
+// random forest trained on A6000 timings; here a decision tree trained on this
+// repo's own B200 sweep is compiled in (decider_model.h).
+// Before a model exists a rule derived from the paper's observations is used:
+//   V = 2 iff PR_2 < 0.30      (T1: V = 2 wins at PR 26.8-30.6 %,
+//                               loses at 47.8-49 %)
+//   S = 1 iff d_max > 8 d^     (balancing pays on skewed degrees)
+//   F: smallest coarsening whose row group fits in a warp with no MAC-job gap
+//      (Eq. 1 generalised to 4G lanes).
+#include <cmath>
+
+#include "decider_model.h"
+#include "pspmm.h"
+
+namespace {
+
+int ceil_pow2(int x) {
+  int p = 1;
+  while (p < x && p < 32) p <<= 1;
+  return p;
+}
+
+// float4 columns per lane F and lanes G covering K with the least waste.
+void pick_fg(int K, int F_hint, int *F, int *G) {
+  const int q = (K + 3) / 4;  // float4 columns (scalar path ignores F)
+  if (F_hint >= 1 && F_hint <= 8) {
+    *F = F_hint;
+    *G = ceil_pow2((q + F_hint - 1) / F_hint);
+    return;
+  }
+  int bestF = 1, bestG = ceil_pow2(q), bestWaste = 1 << 30;
+  for (int f = 1; f <= 8; ++f) {
+    const int g = ceil_pow2((q + f - 1) / f);
+    const int cover = g * f;
+    const int passes = (q + cover - 1) / cover;
+    const int waste = passes * cover - q;
+    // prefer zero waste, then one pass, then the smallest F (fewer registers)
+    const int score = waste * 16 + (passes - 1) * 4;
+    if (score < bestWaste) {
+      bestWaste = score;
+      bestF = f;
+      bestG = g;
+    }
+  }
+  *F = bestF;
+  *G = bestG;
+}
+
+double feature_value(const pspmm_features *f, int idx, int K) {
+  const double *v = reinterpret_cast<const double *>(f);
+  if (idx >= 0 && idx < 16) return v[idx];
+  return std::log2((double)K);
+}
+
+}  // namespace
+
+extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
+                                            pspmm_config *out) {
+  if (!f || !out || K < 1) return PSPMM_ERR_INVALID_ARG;
+  if (!(f->nnz > 0)) return PSPMM_ERR_EMPTY;
+  pspmm_config c{};
+  c.omega = 32;
+  c.sg_override = 0;
+  c.mode = 0;
+  int F_hint = 0;
+#if PSPMM_DECIDER_TRAINED
+  int node = 0;
+  while (pspmm_model::kFeature[node] >= 0) {
+    const double x = feature_value(f, pspmm_model::kFeature[node], K);
+    node = x <= pspmm_model::kThreshold[node] ? pspmm_model::kLeft[node]
+                                              : pspmm_model::kRight[node];
+  }
+  c.V = pspmm_model::kLabel[node][0];
+  c.S = pspmm_model::kLabel[node][1];
+  c.W = pspmm_model::kLabel[node][2];
+  F_hint = pspmm_model::kLabel[node][3];
+#else
+  (void)feature_value;
+  c.V = f->pr2 < 0.30 ? 2 : 1;
+  c.S = f->d_max > 8.0 * f->d_hat ? 1 : 0;
+  c.W = 4;
+#endif
+  pick_fg(K, F_hint, &c.F, &c.G);
+  *out = c;
+  return PSPMM_OK;
+}

@@ -1,0 +1,123 @@
+"""Multi-GPU path: nnz-balanced contiguous row
+shards of A, one process per GPU, and an all-gather of B before every SpMM —
+the GNN-layer pattern where layer l's output rows become layer l+1's B rows.
+
+Host logic (shard plan, column remap into the padded all-gather layout) is in
+the C library (pspmm_shard_plan / pspmm_shard_extract); the collective is
+torch.distributed (NCCL over NVLink on the B200 box, gloo in the CPU tests);
+the compute is pspmm_spmm_run on the rank's PCSR.  This module never imports
+the oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import api
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    bounds: np.ndarray   # P + 1 row bounds (int64)
+    n_max: int           # padded rows per rank in the gathered B
+    rowptr: np.ndarray   # local CSR, rows bounds[r]..bounds[r+1]
+    colidx: np.ndarray   # columns remapped to owner * n_max + offset
+    val: np.ndarray
+
+    @property
+    def lo(self) -> int:
+        return int(self.bounds[self.rank])
+
+    @property
+    def hi(self) -> int:
+        return int(self.bounds[self.rank + 1])
+
+    @property
+    def rows(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def n_cols(self) -> int:
+        return self.world * self.n_max
+
+
+def make_shard(rowptr, colidx, val, world: int, rank: int, align: int = 2) -> Shard:
+    """Row shard of rank `rank` (align = panel height so V = 2 panels never
+    straddle two ranks)."""
+    bounds = api.pspmm_shard_plan(rowptr, world, align)
+    lrp, lci, lvl, n_max = api.pspmm_shard_extract(rowptr, colidx, val, world, bounds, rank)
+    return Shard(rank, world, bounds, n_max, lrp, lci, lvl)
+
+
+def pad_rows(x_local, n_max: int):
+    """Pad this rank's B rows to n_max (all-gather needs equal counts)."""
+    import torch
+    if x_local.shape[0] == n_max:
+        return x_local
+    out = torch.zeros((n_max,) + tuple(x_local.shape[1:]), dtype=x_local.dtype,
+                      device=x_local.device)
+    out[: x_local.shape[0]] = x_local
+    return out
+
+
+def all_gather_rows(x_padded, out=None, group=None):
+    """B_full[g * n_max + i] = rank g's row i.  NCCL: one
+    all_gather_into_tensor; gloo (CPU tests): all_gather into a list."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if out is None:
+        out = torch.empty((world * x_padded.shape[0],) + tuple(x_padded.shape[1:]),
+                          dtype=x_padded.dtype, device=x_padded.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, x_padded, group=group)
+    else:
+        parts = list(out.split(x_padded.shape[0]))
+        dist.all_gather(parts, x_padded, group=group)
+    return out
+
+
+def local_rows(x_full, shard: Shard):
+    """This rank's rows of a gathered matrix (inverse of the padding)."""
+    start = shard.rank * shard.n_max
+    return x_full[start:start + shard.rows]
+
+
+def unpad_gathered(x_full, bounds, n_max: int):
+    """Gathered (P n_max) x K -> the n x K matrix in original row order."""
+    import torch
+    parts = [x_full[g * n_max: g * n_max + int(bounds[g + 1] - bounds[g])]
+             for g in range(len(bounds) - 1)]
+    return torch.cat(parts, 0)
+
+
+class ShardedSpmm:
+    """One rank's state for C_r = A[r-rows, :] . B (B gathered every step)."""
+
+    def __init__(self, shard: Shard, K: int, cfg: api.Config | None = None, device="cuda",
+                 stream=None):
+        import torch
+        self.shard = shard
+        self.K = K
+        rp = torch.from_numpy(shard.rowptr).to(device)
+        ci = torch.from_numpy(shard.colidx if len(shard.colidx) else np.zeros(1, np.int32)).to(device)
+        vl = torch.from_numpy(shard.val if len(shard.val) else np.zeros(1, np.float32)).to(device)
+        nnz = int(shard.rowptr[-1])
+        if cfg is None:
+            cfg = api.Config(W=4, F=1, V=1, S=1)
+        self.cfg = cfg
+        self.A = api.pspmm_pcsr_build(shard.rows, nnz, rp, ci, vl, cfg.V, cfg.S, cfg.omega,
+                                      cfg.sg_override, stream, n_cols=shard.n_cols)
+        self.B_full = torch.empty((shard.n_cols, K), dtype=torch.float32, device=device)
+        self.C = torch.empty((shard.n_max, K), dtype=torch.float32, device=device)
+        self.C[shard.rows:].zero_()
+
+    def step(self, B_padded, stream=None, group=None):
+        """All-gather the padded B shards, then the local SpMM.  Returns the
+        padded local C (the next layer's B shard)."""
+        all_gather_rows(B_padded, self.B_full, group)
+        self.A.run(self.B_full, self.C, self.cfg, stream)
+        return self.C
