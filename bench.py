@@ -325,6 +325,8 @@ def main():
     ap.add_argument("--headline-only", action="store_true",
                     help="skip the per-config table of the other four workloads")
     ap.add_argument("--no-cusparse", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to rehearse the N>1 flow on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -337,9 +339,13 @@ def main():
 
     import torch
     import torch.distributed as dist
+    local_rank = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:  # single-GPU rehearsal of the multi-rank flow (not a measurement)
+            dist.init_process_group("gloo")
     stream = torch.cuda.Stream()
     flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
@@ -433,6 +439,16 @@ def main():
         print(json.dumps(line), flush=True)
 
 
+def max_over_ranks(vals):
+    """Element-wise max over ranks (device tensor on NCCL, host on gloo)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
 def run_sharded(g, args, world, rank, stream, flush, sampler):
     """N > 1: this rank's row shard; step = all-gather(B) + local SpMM."""
     import torch
@@ -465,9 +481,7 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
         tk = time_steps(kernel_only, args.steps, 2, flush, stream)
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([float(np.mean(ts)), float(np.mean(tk))], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, kms = float(t[0]), float(t[1])
+    ms, kms = max_over_ranks([float(np.mean(ts)), float(np.mean(tk))])
     nnz_loc = int(sh.rowptr[-1])
     R = algorithmic_bytes(sh.rows, sh.n_cols, nnz_loc, K)
     # e2e: pinned host B shard -> device, all-gather, SpMM, D2H of the C shard
@@ -482,9 +496,7 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
 
     with torch.cuda.stream(stream):
         te = time_steps(e2e_step, max(3, min(args.steps, 10)), 2, flush, stream)
-    te_t = torch.tensor([float(np.mean(te))], device="cuda")
-    dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
-    me = float(te_t[0])
+    (me,) = max_over_ranks([float(np.mean(te))])
     e2e = {"value": 2.0 * g.nnz * K / (me * 1e-3) / 1e9, "unit": "GFLOP/s",
            "h2d_bytes_per_step": int(hB.numel() * 4), "d2h_bytes_per_step": int(hC.numel() * 4),
            "ms_per_step": me, "path": "rank shard: H2D B rows, all-gather, spmm, D2H C rows"}

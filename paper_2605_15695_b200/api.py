@@ -16,6 +16,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpspmm.so")
+# tools/variants.py experiments may point at another build of the same sources
+LIB_PATH = os.environ.get("PSPMM_LIB", LIB_PATH)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -46,11 +46,11 @@ def _stale(target, inputs):
     return any(os.path.getmtime(i) > t for i in inputs)
 
 
-def _compile(src, verbose=False):
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(src, verbose=False, defines=(), objdir=None):
+    obj = os.path.join(objdir or BUILD, os.path.basename(src) + ".o")
     if not _stale(obj, [src] + _deps()):
         return obj
-    cmd = [NVCC] + ARCH + COMMON + ["-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + COMMON + [f"-D{d}" for d in defines] + ["-c", src, "-o", obj]
     if verbose and src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -84,6 +84,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if base_objs and (force or _stale(LIB_CUSPARSE, base_objs)):
         _link(base_objs, LIB_CUSPARSE, ["-lcusparse"])
     return LIB
+
+
+def build_variant(name: str, defines) -> str:
+    """Same sources with extra -D flags (e.g. a register budget) into
+    paper_2605_15695_b200/variants/libpspmm_<name>.so (experiments only)."""
+    objdir = os.path.join(ROOT, "build", f"obj_{name}")
+    os.makedirs(objdir, exist_ok=True)
+    out_dir = os.path.join(PKG, "variants")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, f"libpspmm_{name}.so")
+    prod, _ = _sources()
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, False, defines, objdir), prod))
+    if _stale(out, objs):
+        _link(objs, out)
+    return out
 
 
 if __name__ == "__main__":

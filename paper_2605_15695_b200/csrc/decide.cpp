@@ -22,7 +22,7 @@ int ceil_pow2(int x) {
 }
 
 // float4 columns per lane F and lanes G covering K with the least waste.
-void pick_fg(int K, int F_hint, int *F, int *G) {
+[[maybe_unused]] void pick_fg(int K, int F_hint, int *F, int *G) {
   const int q = (K + 3) / 4;  // float4 columns (scalar path ignores F)
   if (F_hint >= 1 && F_hint <= 8) {
     *F = F_hint;
@@ -63,7 +63,6 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
   c.omega = 32;
   c.sg_override = 0;
   c.mode = 0;
-  int F_hint = 0;
 #if PSPMM_DECIDER_TRAINED
   int node = 0;
   while (pspmm_model::kFeature[node] >= 0) {
@@ -74,14 +73,23 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
   c.V = pspmm_model::kLabel[node][0];
   c.S = pspmm_model::kLabel[node][1];
   c.W = pspmm_model::kLabel[node][2];
-  F_hint = pspmm_model::kLabel[node][3];
+  c.F = pspmm_model::kLabel[node][3];
+  {
+    // G from the label's column-pass count P: the smallest power of two with
+    // 4 G F P >= K (capped at 32 lanes)
+    const int P = pspmm_model::kLabel[node][4];
+    const int q = (K + 3) / 4;
+    c.G = ceil_pow2((q + c.F * P - 1) / (c.F * P));
+  }
+  *out = c;
+  return PSPMM_OK;
 #else
   (void)feature_value;
   c.V = f->pr2 < 0.30 ? 2 : 1;
   c.S = f->d_max > 8.0 * f->d_hat ? 1 : 0;
   c.W = 4;
-#endif
-  pick_fg(K, F_hint, &c.F, &c.G);
+  pick_fg(K, 0, &c.F, &c.G);
   *out = c;
   return PSPMM_OK;
+#endif
 }

@@ -74,6 +74,13 @@ def all_gather_rows(x_padded, out=None, group=None):
                           dtype=x_padded.dtype, device=x_padded.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, x_padded, group=group)
+    elif x_padded.is_cuda:
+        # gloo (CPU tests / single-GPU rehearsal of the multi-rank bench):
+        # stage through host memory
+        host = torch.empty((world * x_padded.shape[0],) + tuple(x_padded.shape[1:]),
+                           dtype=x_padded.dtype)
+        dist.all_gather(list(host.split(x_padded.shape[0])), x_padded.cpu(), group=group)
+        out.copy_(host)
     else:
         parts = list(out.split(x_padded.shape[0]))
         dist.all_gather(parts, x_padded, group=group)

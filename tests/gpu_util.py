@@ -37,7 +37,8 @@ _cache = {}
 
 
 def oracle_ref(g, B, key=None):
-    k = (key, B.shape) if key is not None else None
+    # the fingerprint of B guards against two tests sharing a key with different B
+    k = (key, B.shape, B.ravel()[:64].tobytes(), float(B.sum())) if key is not None else None
     if k is not None and k in _cache:
         return _cache[k]
     ref = oracle.spmm(g.rowptr, g.colidx, g.val, B, threads=8)

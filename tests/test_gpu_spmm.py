@@ -97,7 +97,7 @@ def test_decided_and_alternative_configs(name, K):
     api = _api()
     g = graph(name)
     B = gen.dense(g.n, K, 40 + K)
-    ref, mag = oracle_ref(g, B, key=(name, K))
+    ref, mag = oracle_ref(g, B, key=(name, K, "decided"))
     rp, ci, _ = dev(g)
     f = api.pspmm_features_compute(g.n, g.nnz, rp, ci)
     cfg = api.pspmm_decide_config(f, K)
@@ -219,7 +219,7 @@ def test_host_e2e_entry():
     g = graph("products_s")
     K = 128
     B = gen.dense(g.n, K, 81)
-    ref, mag = oracle_ref(g, B, key=("products_s", K))
+    ref, mag = oracle_ref(g, B, key=("products_s", K, "e2e"))
     rp, ci, vl = dev(g)
     cfg = api.Config(V=1, S=1, F=1)
     A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, 1, 1)
