@@ -55,7 +55,7 @@ typedef enum {
 
 /*
  * <W, F, V, S> of P:173 plus the build-specific knobs.
- *  W  warps per CTA: 1, 2, 4, 8 or 16.
+ *  W  warps per CTA: 1, 2, 4 or 8.
  *  F  thread-coarsening factor, in B200 units: the number of
  *     128-bit (4 x fp32) accumulators a lane keeps per output row, i.e. a
  *     row group covers 4.G.F columns of C per pass.  1 .. 8.

@@ -53,8 +53,8 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
   if (cfg.V != A->V || cfg.S != A->S || cfg.omega != A->omega)
     PSPMM_FAIL(PSPMM_ERR_CONFIG_MISMATCH, "spmm_run: cfg.V/S/omega differ from the PCSR handle");
   if (cfg.mode != 0) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: only mode 0 is implemented");
-  if (!(cfg.W == 1 || cfg.W == 2 || cfg.W == 4 || cfg.W == 8 || cfg.W == 16))
-    PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: W must be 1, 2, 4, 8 or 16");
+  if (!(cfg.W == 1 || cfg.W == 2 || cfg.W == 4 || cfg.W == 8))
+    PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: W must be 1, 2, 4 or 8");
   if (cfg.W * 32 > PSPMM_MAX_THREADS)
     PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: W exceeds this build's launch bounds");
   if (cfg.F < 1 || cfg.F > 8)

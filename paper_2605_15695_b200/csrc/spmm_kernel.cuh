@@ -189,12 +189,13 @@ __device__ __forceinline__ void mac_tile(const char *__restrict__ bptr, uint32_t
 }
 
 // Register budget: PSPMM_MAX_THREADS x PSPMM_MIN_BLOCKS threads per SM
-// (512 x 1 -> up to 128 registers; tools/variants.py builds other budgets).
+// 256 x 3 -> at most 85 registers, 24 warps per SM: the best of the budgets
+// A/B-tested on B200 (profiles/r01/ab_variants.md); tools/variants.py builds others.
 #ifndef PSPMM_MAX_THREADS
-#define PSPMM_MAX_THREADS 512
+#define PSPMM_MAX_THREADS 256
 #endif
 #ifndef PSPMM_MIN_BLOCKS
-#define PSPMM_MIN_BLOCKS 1
+#define PSPMM_MIN_BLOCKS 3
 #endif
 
 template <int V, int S, int F, int G, bool VEC>

@@ -59,7 +59,7 @@ def test_decider_returns_valid_config(K):
     from paper_2605_15695_b200 import api
     for pr2, dmax in [(0.1, 10.0), (0.45, 5000.0)]:
         c = api.pspmm_decide_config(dict(FEATS, pr2=pr2, d_max=dmax), K)
-        assert c.V in (1, 2) and c.S in (0, 1) and c.W in (1, 2, 4, 8, 16)
+        assert c.V in (1, 2) and c.S in (0, 1) and c.W in (1, 2, 4, 8)
         assert 1 <= c.F <= 8 and c.G in (1, 2, 4, 8, 16, 32) and c.mode == 0 and c.omega == 32
         # pure: same input, same output
         assert api.pspmm_decide_config(dict(FEATS, pr2=pr2, d_max=dmax), K).as_dict() == c.as_dict()

@@ -102,7 +102,7 @@ def test_decided_and_alternative_configs(name, K):
     f = api.pspmm_features_compute(g.n, g.nnz, rp, ci)
     cfg = api.pspmm_decide_config(f, K)
     cfgs = [cfg] + [api.Config(W=W, F=cfg.F, V=V, S=S, G=cfg.G)
-                    for (V, S), W in zip(itertools.product((1, 2), (0, 1)), (1, 2, 8, 16))]
+                    for (V, S), W in zip(itertools.product((1, 2), (0, 1)), (1, 2, 4, 8))]
     for c in cfgs:
         C, _ = run(g, B, c)
         assert_parity(C, ref, mag, f"{name} K{K} {c}")

@@ -1,0 +1,41 @@
+#!/bin/bash
+# One GPU session: tests, smoke, bench (+ launch list), ncu captures of the
+# engine on every workload, and (optionally) the decider sweep.
+# usage: bash tools/gpu_round.sh [tests] [bench] [ncu] [sweep] [corpus]
+set -u
+export PSPMM_GEN_CACHE=/tmp/pspmm_gen_cache
+O=gpurun_out
+mkdir -p $O
+want() { for a in "${ARGS[@]}"; do [ "$a" = "$1" ] && return 0; done; return 1; }
+ARGS=("$@")
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,driver_version --format=csv > $O/gpu.txt 2>&1
+(nproc; lscpu | grep "Model name") > $O/host.txt 2>&1
+
+if want tests; then
+  timeout 2400 python -m pytest tests -m gpu -q --maxfail=25 > $O/pytest_gpu.log 2>&1
+  echo "pytest exit $?" >> $O/pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+  echo "smoke exit $?" >> $O/smoke.log
+fi
+if want bench; then
+  timeout 1500 python bench.py > $O/bench.log 2>&1
+  echo "bench exit $?" >> $O/bench.log
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+      --log-file $O/launches.csv python bench.py --steps 5 --warmup 3 --headline-only --no-cusparse \
+      > $O/bench_ncu.log 2>&1
+fi
+if want ncu; then
+  for w in reddit roadnet products proteins cora; do
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm_kernel -s 1 -c 1 \
+        -o $O/prof_$w -f python tools/run_kernel.py --workload $w --iters 2 > $O/ncu_$w.log 2>&1
+  done
+fi
+if want sweep; then
+  timeout 1800 python tools/sweep.py --workloads cora,roadnet,reddit,proteins,products --iters 5 \
+      --out $O/sweep_workloads.json > $O/sweep_workloads.log 2>&1
+fi
+if want corpus; then
+  timeout 2400 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 \
+      --out $O/sweep_corpus.json > $O/sweep_corpus.log 2>&1
+fi
+echo done > $O/round_done.txt
