@@ -66,8 +66,13 @@ typedef enum {
  *  sg_override  0 = Split Granularity from Eq. 3; > 0 forces SG (c-18).
  *  G  lanes per row group (1, 2, 4, 8, 16, 32); 0 = derived from K and F
  *     as the smallest power of two with 4.G.F >= K (capped at 32).
- *  mode  0 = CUDA-core engine (the only mode implemented; 1 is reserved for
- *     the dense-panel tensor-core path and returns PSPMM_ERR_UNSUPPORTED).
+ *  mode  0 = CUDA-core engine, B rows gathered with 128-bit loads into
+ *     registers (any K, any layout; W, F, G apply);
+ *     2 = CUDA-core engine, B rows gathered by TMA tile::gather4 into a
+ *     shared-memory ring per warp (needs K % 32 == 0, ld % 4 == 0, 16-B
+ *     aligned B and C, else PSPMM_ERR_UNSUPPORTED; only W applies);
+ *     1 is reserved for a dense-panel tensor-core path and returns
+ *     PSPMM_ERR_UNSUPPORTED.
  * For pspmm_pcsr_build only V, S, omega and sg_override matter.
  */
 typedef struct {

@@ -18,7 +18,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(ROOT, "build", "obj")
+# object files live outside the tree (only the .so files are in-tree and travel)
+OBJROOT = os.environ.get("PSPMM_OBJ_DIR", os.path.join("/tmp", "pspmm_build"))
+BUILD = os.path.join(OBJROOT, "obj")
 LIB = os.path.join(PKG, "libpspmm.so")
 LIB_CUSPARSE = os.path.join(PKG, "libpspmm_cusparse.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -89,7 +91,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 def build_variant(name: str, defines) -> str:
     """Same sources with extra -D flags (e.g. a register budget) into
     paper_2605_15695_b200/variants/libpspmm_<name>.so (experiments only)."""
-    objdir = os.path.join(ROOT, "build", f"obj_{name}")
+    objdir = os.path.join(OBJROOT, f"obj_{name}")
     os.makedirs(objdir, exist_ok=True)
     out_dir = os.path.join(PKG, "variants")
     os.makedirs(out_dir, exist_ok=True)

@@ -71,6 +71,11 @@ pspmm_status panel_counts_v2(int64_t n_rows, const int32_t *d_rowptr, const int3
 pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
                       int64_t ldc, const pspmm_config &cfg, cudaStream_t stream);
 
+// spmm_tma.cu (engine mode 2)
+bool tma_supported(int32_t K, int64_t ldb, int64_t ldc, const float *d_B, const float *d_C);
+pspmm_status run_spmm_tma(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
+                          float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream);
+
 // features.cu
 pspmm_status compute_features(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                               const int32_t *d_colidx, int32_t omega, cudaStream_t stream,

@@ -52,7 +52,8 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
     PSPMM_FAIL(PSPMM_ERR_DIM_MISMATCH, "spmm_run: need K >= 1, ldb >= K, ldc >= K");
   if (cfg.V != A->V || cfg.S != A->S || cfg.omega != A->omega)
     PSPMM_FAIL(PSPMM_ERR_CONFIG_MISMATCH, "spmm_run: cfg.V/S/omega differ from the PCSR handle");
-  if (cfg.mode != 0) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: only mode 0 is implemented");
+  if (cfg.mode != 0 && cfg.mode != 2)
+    PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: mode must be 0 (LDG engine) or 2 (TMA gather)");
   if (!(cfg.W == 1 || cfg.W == 2 || cfg.W == 4 || cfg.W == 8))
     PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: W must be 1, 2, 4 or 8");
   if (cfg.W * 32 > PSPMM_MAX_THREADS)
@@ -84,8 +85,15 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
     G = ceil_pow2(K);
     cols_per_pass = G;
   }
-  KernelFn fn = pick_kernel(A->V, A->S, vec, F, G);
-  if (!fn) PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: no kernel instance for this config");
+  KernelFn fn = nullptr;
+  if (cfg.mode == 2) {
+    if (!tma_supported(K, ldb, ldc, d_B, d_C))
+      PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
+                 "spmm_run mode 2: needs K % 32 == 0, ld % 4 == 0 and 16-B aligned B and C");
+  } else {
+    fn = pick_kernel(A->V, A->S, vec, F, G);
+    if (!fn) PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: no kernel instance for this config");
+  }
 
   if (A->S == 1 && A->num_split > 0) {
     int64_t total = A->num_split * A->V * (int64_t)K;
@@ -94,6 +102,7 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
                                                    ldc);
     PSPMM_CUDA_TRY(cudaGetLastError());
   }
+  if (cfg.mode == 2) return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream);
 
   SpmmArgs args;
   args.rowptr = A->d_rowptr;

@@ -1,0 +1,54 @@
+"""bench.py end to end on the GPU (small workload): the single-GPU JSON line
+carries the contract keys, and the N>1 flow (row shards + all-gather + max
+over ranks) runs as a 2-rank rehearsal on one GPU with the gloo backend
+(NCCL cannot put two ranks on one device)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+        "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches",
+        "clocks")
+
+
+def _run(cmd, env=None):
+    e = dict(os.environ, **(env or {}))
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=e)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_single_gpu_line():
+    out = _run([sys.executable, "bench.py", "--workload", "cora", "--steps", "3", "--warmup", "3",
+                "--headline-only"])
+    for k in KEYS:
+        assert k in out, k
+    assert out["n_gpus"] == 1 and out["value"] > 0 and out["gpu_launches"] >= 3
+    assert set(out["roofline"]) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
+    assert set(out["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
+    assert out["cpu_baseline"]["kind"] == "oracle" and out["cpu_baseline"]["cores"] >= 1
+
+
+def test_bench_two_rank_rehearsal_gloo():
+    out = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py",
+                "--workload", "cora", "--steps", "3", "--warmup", "3", "--headline-only",
+                "--dist-backend", "gloo"])
+    assert out["n_gpus"] == 2 and out["value"] > 0
+    assert "row shards" in out["config"]["parallelism"]
+
+
+def test_bench_reference_arm():
+    out = _run([sys.executable, "bench.py", "--impl", "reference", "--workload", "cora",
+                "--steps", "2", "--warmup", "1"])
+    assert out["impl"] == "reference" and out["value"] > 0
+    assert out["e2e"]["h2d_bytes_per_step"] == 0

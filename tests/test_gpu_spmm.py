@@ -108,6 +108,30 @@ def test_decided_and_alternative_configs(name, K):
         assert_parity(C, ref, mag, f"{name} K{K} {c}")
 
 
+@pytest.mark.parametrize("V,S", [(1, 0), (1, 1), (2, 0), (2, 1)])
+@pytest.mark.parametrize("K", [32, 64, 96, 128, 256, 512])
+@pytest.mark.parametrize("W", [1, 4, 8])
+def test_tma_gather_engine(V, S, K, W):
+    """Engine mode 2 (TMA tile::gather4 into shared memory)."""
+    api = _api()
+    g = main_graph()
+    B = gen.dense(g.n, K, 300 + K)
+    ref, mag = oracle_ref(g, B, key=("main_tma", K))
+    if W * 8 * (4 * min(K, 256) * 4) > 227 * 1024:  # W warps x 8 slots x 4 rows
+        pytest.skip("ring does not fit shared memory at this W")
+    C, _ = run(g, B, api.Config(W=W, V=V, S=S, mode=2))
+    assert_parity(C, ref, mag, f"tma V{V} S{S} K{K} W{W}")
+
+
+def test_tma_engine_rejects_unsupported_K():
+    api = _api()
+    g = graph("cora")
+    B = gen.dense(g.n, 20, 1)
+    with pytest.raises(api.PspmmError) as e:
+        run(g, B, api.Config(V=1, S=0, mode=2))
+    assert e.value.status == api.PSPMM_ERR_UNSUPPORTED
+
+
 def test_identity_exact_all_corners():
     api = _api()
     n = 1537

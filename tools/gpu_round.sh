@@ -25,10 +25,15 @@ if want bench; then
       > $O/bench_ncu.log 2>&1
 fi
 if want ncu; then
+  # full captures are summarised here (JSON) and only the headline report is
+  # kept: gpurun_out/ must stay under 64 MiB or nothing comes back
   for w in reddit roadnet products proteins cora; do
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm_kernel -s 1 -c 1 \
-        -o $O/prof_$w -f python tools/run_kernel.py --workload $w --iters 2 > $O/ncu_$w.log 2>&1
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm -s 1 -c 1 \
+        -o /tmp/prof_$w -f python tools/run_kernel.py --workload $w --iters 2 > $O/ncu_$w.log 2>&1
+    python tools/ncu_summary.py /tmp/prof_$w.ncu-rep --json $O/ncu_$w.json > /dev/null 2>&1
+    ncu -i /tmp/prof_$w.ncu-rep --page details --csv > $O/ncu_${w}_details.csv 2>/dev/null
   done
+  cp /tmp/prof_reddit.ncu-rep $O/ 2>/dev/null
 fi
 if want sweep; then
   timeout 1800 python tools/sweep.py --workloads cora,roadnet,reddit,proteins,products --iters 5 \
@@ -38,4 +43,6 @@ if want corpus; then
   timeout 2400 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 \
       --out $O/sweep_corpus.json > $O/sweep_corpus.log 2>&1
 fi
+# never let gpurun_out/ exceed the 64 MiB merge limit
+if [ "$(du -sm $O | cut -f1)" -gt 56 ]; then rm -f $O/*.ncu-rep; fi
 echo done > $O/round_done.txt

@@ -18,7 +18,7 @@ def main(argv):
     for spec in argv:
         if spec.startswith("git:"):
             rev, name = spec[4:].split("=")
-            src_dir = os.path.join(ROOT, "build", f"src_{name}")
+            src_dir = os.path.join(build_ext.OBJROOT, f"src_{name}")
             shutil.rmtree(src_dir, ignore_errors=True)
             shutil.copytree(build_ext.CSRC, src_dir)
             old = subprocess.check_output(
