@@ -22,7 +22,7 @@ int ceil_pow2(int x) {
 }
 
 // float4 columns per lane F and lanes G covering K with the least waste.
-[[maybe_unused]] void pick_fg(int K, int F_hint, int *F, int *G) {
+void pick_fg(int K, int F_hint, int *F, int *G) {
   const int q = (K + 3) / 4;  // float4 columns (scalar path ignores F)
   if (F_hint >= 1 && F_hint <= 8) {
     *F = F_hint;
@@ -70,14 +70,21 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
     node = x <= pspmm_model::kThreshold[node] ? pspmm_model::kLeft[node]
                                               : pspmm_model::kRight[node];
   }
-  c.V = pspmm_model::kLabel[node][0];
-  c.S = pspmm_model::kLabel[node][1];
-  c.W = pspmm_model::kLabel[node][2];
-  c.F = pspmm_model::kLabel[node][3];
-  {
+  const int *lab = pspmm_model::kLabel[node];
+  c.mode = lab[0];
+  c.V = lab[1];
+  c.S = lab[2];
+  c.W = lab[3];
+  if (c.mode == 2 && K % 32 != 0) c.mode = 0;  // TMA engine needs K % 32 == 0
+  if (c.mode == 2) {
+    pick_fg(K, 0, &c.F, &c.G);  // unused by mode 2; a valid mode-0 fallback
+  } else if (lab[0] == 2) {
+    pick_fg(K, 0, &c.F, &c.G);
+  } else {
     // G from the label's column-pass count P: the smallest power of two with
     // 4 G F P >= K (capped at 32 lanes)
-    const int P = pspmm_model::kLabel[node][4];
+    c.F = lab[4];
+    const int P = lab[5];
     const int q = (K + 3) / 4;
     c.G = ceil_pow2((q + c.F * P - 1) / (c.F * P));
   }

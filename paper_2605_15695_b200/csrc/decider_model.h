@@ -12,6 +12,6 @@ constexpr int kFeature[kNodes] = {-1};
 constexpr double kThreshold[kNodes] = {0.0};
 constexpr int kLeft[kNodes] = {-1};
 constexpr int kRight[kNodes] = {-1};
-// leaf label: {V, S, W, F, P (column passes)}
-constexpr int kLabel[kNodes][5] = {{1, 0, 4, 1, 1}};
+// leaf label: {mode, V, S, W, F, P (column passes)}
+constexpr int kLabel[kNodes][6] = {{0, 1, 0, 4, 1, 1}};
 }  // namespace pspmm_model

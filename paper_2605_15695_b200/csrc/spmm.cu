@@ -118,7 +118,11 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
   args.K = K;
   const int threads = cfg.W * 32;
   const int64_t groups_per_block = threads / G;
-  const int64_t bx = (A->num_chunks + groups_per_block - 1) / groups_per_block;
+  // groups loop over units (grid-stride): cap the grid at PSPMM_WAVES waves of
+  // resident blocks so each group pipelines several units
+  int64_t bx = (A->num_chunks + groups_per_block - 1) / groups_per_block;
+  const int64_t resident = std::min<int64_t>(32, (PSPMM_MAX_THREADS * PSPMM_MIN_BLOCKS) / threads);
+  if (PSPMM_WAVES > 0) bx = std::min<int64_t>(bx, (int64_t)num_sms() * resident * PSPMM_WAVES);
   const int64_t by = (K + cols_per_pass - 1) / cols_per_pass;
   if ((uint64_t)ldb * 4 >= (1ull << 32))
     PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: ldb * 4 bytes must be < 2^32");

@@ -1,0 +1,27 @@
+"""compute-sanitizer memcheck / racecheck / synccheck over a tiny run of every
+native kernel (SURVEY §4 "Sanitizers")."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.fail("compute-sanitizer not found")
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "17",
+                        "--kernel-name", "kns=pspmm",  # our kernels (namespace pspmm), not torch's
+                        sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "sanitize run ok" in out
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]

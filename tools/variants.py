@@ -20,10 +20,14 @@ def main(argv):
             rev, name = spec[4:].split("=")
             src_dir = os.path.join(build_ext.OBJROOT, f"src_{name}")
             shutil.rmtree(src_dir, ignore_errors=True)
-            shutil.copytree(build_ext.CSRC, src_dir)
-            old = subprocess.check_output(
-                ["git", "show", f"{rev}:paper_2605_15695_b200/csrc/spmm.cu"], cwd=ROOT)
-            open(os.path.join(src_dir, "spmm.cu"), "wb").write(old)
+            os.makedirs(src_dir)
+            # the whole csrc/ tree as of `rev`
+            files = subprocess.check_output(
+                ["git", "ls-tree", "--name-only", rev, "paper_2605_15695_b200/csrc/"],
+                cwd=ROOT, text=True).split()
+            for f in files:
+                blob = subprocess.check_output(["git", "show", f"{rev}:{f}"], cwd=ROOT)
+                open(os.path.join(src_dir, os.path.basename(f)), "wb").write(blob)
             saved = build_ext.CSRC
             build_ext.CSRC = src_dir
             try:
