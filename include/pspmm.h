@@ -186,9 +186,12 @@ pspmm_status pspmm_spmm_run(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t
 /*
  * End-to-end variant for host-resident B and C (bench.py "e2e"): copies
  * h_B (n x K, ldb) into the caller's device staging buffer d_Bbuf (same
- * layout), runs pspmm_spmm_run into d_Cbuf (ldc), copies d_Cbuf back into
- * h_C, and synchronises `stream`.  h_B / h_C should be pinned for the
- * copies to be asynchronous.
+ * layout), runs the engine into d_Cbuf (ldc) in 8 slices of units cut at
+ * panel boundaries, copies each slice's rows of C back into h_C on an
+ * internal second stream as soon as that slice is done (so the D2H copy
+ * overlaps the remaining compute), and synchronises `stream`.  h_B / h_C
+ * should be pinned for the copies to be asynchronous.  The first call on a
+ * handle creates its copy stream and events (released by destroy).
  */
 pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, int32_t K,
                                  float *h_C, int64_t ldc, pspmm_config cfg, float *d_Bbuf,

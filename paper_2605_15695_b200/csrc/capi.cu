@@ -133,6 +133,12 @@ void pspmm_pcsr_destroy(pspmm_pcsr A) {
   cudaFree(A->d_val);
   cudaFree(A->d_trow);
   cudaFree(A->d_split);
+  if (A->copy_stream) {
+    cudaStreamSynchronize(A->copy_stream);
+    cudaStreamDestroy(A->copy_stream);
+    for (int k = 0; k < kSlices; ++k)
+      if (A->slice_done[k]) cudaEventDestroy(A->slice_done[k]);
+  }
   delete A;
 }
 
@@ -152,15 +158,7 @@ pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, in
     set_error("spmm_run_host: need K >= 1, ldb >= K, ldc >= K");
     return PSPMM_ERR_DIM_MISMATCH;
   }
-  cudaStream_t s = as_stream(stream);
-  PSPMM_CUDA_TRY(cudaMemcpyAsync(d_Bbuf, h_B, (size_t)A->n_cols * ldb * sizeof(float),
-                                 cudaMemcpyHostToDevice, s));
-  pspmm_status st = run_spmm(A, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, s);
-  if (st != PSPMM_OK) return st;
-  PSPMM_CUDA_TRY(cudaMemcpyAsync(h_C, d_Cbuf, (size_t)A->n_rows * ldc * sizeof(float),
-                                 cudaMemcpyDeviceToHost, s));
-  PSPMM_CUDA_TRY(cudaStreamSynchronize(s));
-  return PSPMM_OK;
+  return run_spmm_host(A, h_B, ldb, K, h_C, ldc, cfg, d_Bbuf, d_Cbuf, as_stream(stream));
 }
 
 pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_rowptr,

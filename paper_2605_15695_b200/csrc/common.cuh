@@ -12,6 +12,9 @@
 // derived data that is NOT part of the bit-exact PCSR contract:
 //   d_split  = ids of panels that own more than one chunk (S = 1); their C
 //              rows are zeroed before the chunks accumulate into them.
+//   slice_*  = kSlices + 1 unit / row bounds at panel boundaries, used by the
+//              host entry to overlap the D2H copy of C with the engine.
+constexpr int kSlices = 8;
 struct pspmm_pcsr_s {
   int64_t n_rows = 0, n_cols = 0, num_panels = 0, nnz = 0, nnz_v = 0, num_chunks = 0;
   int64_t sg = 0, rowptr_len = 0, num_split = 0;
@@ -22,6 +25,10 @@ struct pspmm_pcsr_s {
   float *d_val = nullptr;       // nnz_v * V
   int32_t *d_trow = nullptr;    // num_chunks (S = 1)
   int32_t *d_split = nullptr;   // num_split (S = 1)
+  int64_t slice_units[kSlices + 1] = {};
+  int64_t slice_rows[kSlices + 1] = {};
+  cudaStream_t copy_stream = nullptr;  // created lazily by pspmm_spmm_run_host
+  cudaEvent_t slice_done[kSlices] = {};
 };
 
 namespace pspmm {
@@ -74,7 +81,13 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
 // spmm_tma.cu (engine mode 2)
 bool tma_supported(int32_t K, int64_t ldb, int64_t ldc, const float *d_B, const float *d_C);
 pspmm_status run_spmm_tma(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
-                          float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream);
+                          float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
+                          int64_t u0, int64_t u1);
+// host entry: H2D(B), engine in kSlices unit slices, D2H of each slice's C
+// rows on a second stream as soon as the slice is done
+pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32_t K, float *h_C,
+                           int64_t ldc, const pspmm_config &cfg, float *d_Bbuf, float *d_Cbuf,
+                           cudaStream_t stream);
 
 // features.cu
 pspmm_status compute_features(int64_t n, int64_t nnz, const int32_t *d_rowptr,

@@ -14,6 +14,8 @@
 //   S = 1: SG = ceil(nnz_V / (P^ omega)) omega (c-3a) or sg_override;
 //          panel p with L vectors -> max(1, ceil(L/SG)) chunks (c-5) at
 //          offsets 0, SG, 2SG ...; TRow[c] = p.
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -309,6 +311,11 @@ pspmm_status build_pcsr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32
     narrow_kernel<<<grid_for(P + 1, kBlock), kBlock, 0, stream>>>(P + 1, panelptr, A->d_rowptr);
     PSPMM_CUDA_TRY(cudaGetLastError());
     PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
+    for (int k = 0; k <= kSlices; ++k) {
+      const int64_t p = P * k / kSlices;
+      A->slice_units[k] = p;
+      A->slice_rows[k] = std::min<int64_t>(p * V, n_rows);
+    }
     return PSPMM_OK;
   }
 
@@ -352,6 +359,13 @@ pspmm_status build_pcsr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32
   chunk_fill_kernel<<<grid_for(P, kBlock), kBlock, 0, stream>>>(
       P, SG, nnz_v, panelptr, choff, splitoff, A->d_rowptr, A->d_trow, A->d_split);
   PSPMM_CUDA_TRY(cudaGetLastError());
+  // slice bounds at panel boundaries: unit = first chunk of the panel
+  for (int k = 0; k <= kSlices; ++k) {
+    const int64_t p = P * k / kSlices;
+    PSPMM_CUDA_TRY(cudaMemcpyAsync(&A->slice_units[k], choff + p, sizeof(int64_t),
+                                   cudaMemcpyDeviceToHost, stream));
+    A->slice_rows[k] = std::min<int64_t>(p * V, n_rows);
+  }
   PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
   return PSPMM_OK;
 }

@@ -45,8 +45,17 @@ int ceil_pow2(int64_t x) {
 
 }  // namespace
 
-pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
-                      int64_t ldc, const pspmm_config &cfg, cudaStream_t stream) {
+namespace {
+
+// Validated launch plan of one engine call.
+struct Plan {
+  KernelFn fn = nullptr;
+  int threads = 0, G = 1;
+  int64_t by = 1;
+};
+
+pspmm_status make_plan(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
+                       const float *d_C, int64_t ldc, const pspmm_config &cfg, Plan *plan) {
   if (!A || !d_B || !d_C) PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run: null handle or pointer");
   if (K < 1 || ldb < K || ldc < K)
     PSPMM_FAIL(PSPMM_ERR_DIM_MISMATCH, "spmm_run: need K >= 1, ldb >= K, ldc >= K");
@@ -62,16 +71,14 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
     PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: F must be in 1..8 (float4 units)");
   if (cfg.G != 0 && !(pow2(cfg.G) && cfg.G <= 32))
     PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: G must be 0 or a power of two <= 32");
-
-  const int64_t n_rows = A->n_rows;
-  if (A->nnz_v == 0) {
-    int64_t total = n_rows * K;
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
-    zero_all_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(n_rows, K, d_C, ldc);
-    PSPMM_CUDA_TRY(cudaGetLastError());
+  if ((uint64_t)ldb * 4 >= (1ull << 32))
+    PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: ldb * 4 bytes must be < 2^32");
+  if (cfg.mode == 2) {
+    if (!tma_supported(K, ldb, ldc, d_B, d_C))
+      PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
+                 "spmm_run mode 2: needs K % 32 == 0, ld % 4 == 0 and 16-B aligned B and C");
     return PSPMM_OK;
   }
-
   const bool vec = (K % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(d_B) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(d_C) & 15) == 0);
@@ -85,25 +92,39 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
     G = ceil_pow2(K);
     cols_per_pass = G;
   }
-  KernelFn fn = nullptr;
-  if (cfg.mode == 2) {
-    if (!tma_supported(K, ldb, ldc, d_B, d_C))
-      PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
-                 "spmm_run mode 2: needs K % 32 == 0, ld % 4 == 0 and 16-B aligned B and C");
-  } else {
-    fn = pick_kernel(A->V, A->S, vec, F, G);
-    if (!fn) PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: no kernel instance for this config");
-  }
+  plan->fn = pick_kernel(A->V, A->S, vec, F, G);
+  if (!plan->fn) PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: no kernel instance for this config");
+  plan->threads = cfg.W * 32;
+  plan->G = G;
+  plan->by = (K + cols_per_pass - 1) / cols_per_pass;
+  if (plan->by > 65535) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: too many column passes");
+  return PSPMM_OK;
+}
 
-  if (A->S == 1 && A->num_split > 0) {
-    int64_t total = A->num_split * A->V * (int64_t)K;
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
-    zero_split_kernel<<<blocks, 256, 0, stream>>>(A->d_split, A->num_split, A->V, n_rows, K, d_C,
-                                                   ldc);
+// C rows of split panels = 0 (S = 1, c-12); everything else is overwritten.
+pspmm_status prepare_c(const pspmm_pcsr_s *A, int32_t K, float *d_C, int64_t ldc,
+                       cudaStream_t stream) {
+  if (A->nnz_v == 0) {
+    const int64_t total = A->n_rows * K;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+    zero_all_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(A->n_rows, K, d_C, ldc);
+    PSPMM_CUDA_TRY(cudaGetLastError());
+  } else if (A->S == 1 && A->num_split > 0) {
+    const int64_t total = A->num_split * A->V * (int64_t)K;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+    zero_split_kernel<<<blocks, 256, 0, stream>>>(A->d_split, A->num_split, A->V, A->n_rows, K,
+                                                   d_C, ldc);
     PSPMM_CUDA_TRY(cudaGetLastError());
   }
-  if (cfg.mode == 2) return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream);
+  return PSPMM_OK;
+}
 
+// The engine over units [u0, u1).
+pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *d_B,
+                          int64_t ldb, int32_t K, float *d_C, int64_t ldc,
+                          const pspmm_config &cfg, cudaStream_t stream, int64_t u0, int64_t u1) {
+  if (A->nnz_v == 0 || u1 <= u0) return PSPMM_OK;
+  if (cfg.mode == 2) return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1);
   SpmmArgs args;
   args.rowptr = A->d_rowptr;
   args.colidx = A->d_colidx;
@@ -113,23 +134,69 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
   args.C = d_C;
   args.ldb = ldb;
   args.ldc = ldc;
-  args.n_rows = (int32_t)n_rows;
-  args.units = (int32_t)A->num_chunks;
+  args.n_rows = (int32_t)A->n_rows;
+  args.unit_begin = (int32_t)u0;
+  args.units = (int32_t)u1;
+  args.units_total = (int32_t)A->num_chunks;
   args.K = K;
-  const int threads = cfg.W * 32;
-  const int64_t groups_per_block = threads / G;
+  const int64_t groups_per_block = plan.threads / plan.G;
   // groups loop over units (grid-stride): cap the grid at PSPMM_WAVES waves of
   // resident blocks so each group pipelines several units
-  int64_t bx = (A->num_chunks + groups_per_block - 1) / groups_per_block;
-  const int64_t resident = std::min<int64_t>(32, (PSPMM_MAX_THREADS * PSPMM_MIN_BLOCKS) / threads);
+  int64_t bx = (u1 - u0 + groups_per_block - 1) / groups_per_block;
+  const int64_t resident =
+      std::min<int64_t>(32, (PSPMM_MAX_THREADS * PSPMM_MIN_BLOCKS) / plan.threads);
   if (PSPMM_WAVES > 0) bx = std::min<int64_t>(bx, (int64_t)num_sms() * resident * PSPMM_WAVES);
-  const int64_t by = (K + cols_per_pass - 1) / cols_per_pass;
-  if ((uint64_t)ldb * 4 >= (1ull << 32))
-    PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: ldb * 4 bytes must be < 2^32");
-  if (bx > 0x7fffffff || by > 65535)
-    PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: grid too large for this config");
-  fn<<<dim3((unsigned)bx, (unsigned)by), threads, 0, stream>>>(args);
+  if (bx > 0x7fffffff) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: grid too large");
+  plan.fn<<<dim3((unsigned)bx, (unsigned)plan.by), plan.threads, 0, stream>>>(args);
   PSPMM_CUDA_TRY(cudaGetLastError());
+  return PSPMM_OK;
+}
+
+}  // namespace
+
+pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
+                      int64_t ldc, const pspmm_config &cfg, cudaStream_t stream) {
+  Plan plan;
+  pspmm_status st = make_plan(A, d_B, ldb, K, d_C, ldc, cfg, &plan);
+  if (st != PSPMM_OK) return st;
+  st = prepare_c(A, K, d_C, ldc, stream);
+  if (st != PSPMM_OK) return st;
+  return launch_range(A, plan, d_B, ldb, K, d_C, ldc, cfg, stream, 0, A->num_chunks);
+}
+
+pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32_t K, float *h_C,
+                           int64_t ldc, const pspmm_config &cfg, float *d_Bbuf, float *d_Cbuf,
+                           cudaStream_t stream) {
+  if (!A || !h_B || !h_C)
+    PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_host: null handle or host pointer");
+  Plan plan;
+  pspmm_status st = make_plan(A, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, &plan);
+  if (st != PSPMM_OK) return st;
+  if (!A->copy_stream) {
+    PSPMM_CUDA_TRY(cudaStreamCreateWithFlags(&A->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < kSlices; ++k)
+      PSPMM_CUDA_TRY(cudaEventCreateWithFlags(&A->slice_done[k], cudaEventDisableTiming));
+  }
+  PSPMM_CUDA_TRY(cudaMemcpyAsync(d_Bbuf, h_B, (size_t)A->n_cols * ldb * sizeof(float),
+                                 cudaMemcpyHostToDevice, stream));
+  st = prepare_c(A, K, d_Cbuf, ldc, stream);
+  if (st != PSPMM_OK) return st;
+  for (int k = 0; k < kSlices; ++k) {
+    st = launch_range(A, plan, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, stream, A->slice_units[k],
+                      A->slice_units[k + 1]);
+    if (st != PSPMM_OK) return st;
+    PSPMM_CUDA_TRY(cudaEventRecord(A->slice_done[k], stream));
+    PSPMM_CUDA_TRY(cudaStreamWaitEvent(A->copy_stream, A->slice_done[k], 0));
+    const int64_t r0 = A->slice_rows[k], r1 = A->slice_rows[k + 1];
+    if (r1 > r0)
+      PSPMM_CUDA_TRY(cudaMemcpyAsync(h_C + r0 * ldc, d_Cbuf + r0 * ldc,
+                                     (size_t)(r1 - r0) * ldc * sizeof(float),
+                                     cudaMemcpyDeviceToHost, A->copy_stream));
+  }
+  // the caller's stream observes the copies' completion, then the host waits
+  PSPMM_CUDA_TRY(cudaEventRecord(A->slice_done[0], A->copy_stream));
+  PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->slice_done[0], 0));
+  PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
   return PSPMM_OK;
 }
 

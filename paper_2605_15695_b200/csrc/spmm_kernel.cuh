@@ -40,7 +40,7 @@ struct SpmmArgs {
   const float *__restrict__ B;
   float *__restrict__ C;
   int64_t ldb, ldc;
-  int32_t n_rows, units, K;
+  int32_t n_rows, unit_begin, units, units_total, K;  // units = end of this launch's range
 };
 
 // L2 policies: A (colIdx / val) is streamed once -> evict_first and no L1
@@ -197,9 +197,11 @@ __device__ __forceinline__ void mac_tile(const char *__restrict__ bptr, uint32_t
 #ifndef PSPMM_MIN_BLOCKS
 #define PSPMM_MIN_BLOCKS 3
 #endif
-// grid = at most PSPMM_WAVES waves of resident blocks (0 = one group per unit)
+// grid = at most PSPMM_WAVES waves of resident blocks (0 = one group per
+// unit, the default: a grid-stride variant with cross-unit prefetch measured
+// 5-14 % slower, profiles/r01/ab_variants.md)
 #ifndef PSPMM_WAVES
-#define PSPMM_WAVES 4
+#define PSPMM_WAVES 0
 #endif
 
 template <int V, int S, int F, int G, bool VEC>
@@ -220,9 +222,8 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
   const int lane = threadIdx.x & 31;
   const int g = lane / G;
   const int l = lane % G;
-  // grid-stride over units: group (warp, g) takes units first, first + ustride, ...
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t ustride = ((int64_t)gridDim.x * blockDim.x >> 5) * GPW;
+  const int64_t unit = a.unit_begin + warp * GPW + g;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
   const int col0 = blockIdx.y * (G * F * VW);
   const uint64_t pol_a = policy_evict_first();
@@ -239,106 +240,74 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
   const char *bptr = reinterpret_cast<const char *>(a.B + coff[0]);
   const uint32_t stride = (uint32_t)(a.ldb * 4);
 
-  // Software pipeline over units and tiles: rowPtr is loaded two units
-  // ahead, the (colIdx, val) tile one tile ahead — across the unit boundary
-  // too, so short rows (roadNet: ~3 vectors) do not pay the dependent
-  // rowPtr -> colIdx -> B latency chain once per unit.
-  int64_t u = warp * GPW + g;
   int head = 0, tail = 0;
-  if (u < a.units) {
-    head = a.rowptr[u];
-    tail = a.rowptr[u + 1];
+  if (unit < a.units) {
+    head = a.rowptr[unit];
+    tail = a.rowptr[unit + 1];
   }
-  int64_t u1 = u + ustride;
-  int h1 = 0, t1 = 0;
-  if (u1 < a.units) {
-    h1 = a.rowptr[u1];
-    t1 = a.rowptr[u1 + 1];
-  }
+
+  T acc[V][F];
+#pragma unroll
+  for (int k = 0; k < V; ++k)
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[k][f] = zero_v<T>();
+
+  // software pipeline over tiles: the next tile's (colIdx, val) loads are in
+  // flight while the current tile's B rows are gathered
   int mc[M];
   float mv[M][V];
-  bool have = false;  // mc / mv hold the current unit's first tile
-  while (u < a.units) {
-    const int64_t u2 = u1 + ustride;
-    int h2 = 0, t2 = 0;
-    if (u2 < a.units) {
-      h2 = a.rowptr[u2];
-      t2 = a.rowptr[u2 + 1];
-    }
-    if (!have && head < tail) load_tile<V, M, G>(a, head, tail, l, pol_a, mc, mv);
-    have = false;
-
-    T acc[V][F];
+  if (head < tail) load_tile<V, M, G>(a, head, tail, l, pol_a, mc, mv);
+  for (int base = head; base < tail; base += TILE) {
+    int nc[M];
+    float nv[M][V];
+    const bool more = base + TILE < tail;
+    if (more) load_tile<V, M, G>(a, base + TILE, tail, l, pol_a, nc, nv);
+    const int cnt = tail - base;
+    if (cnt >= TILE)
+      mac_tile<V, F, G, M, U, VEC, true>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
+    else
+      mac_tile<V, F, G, M, U, VEC, false>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
+    if (more) {
 #pragma unroll
-    for (int k = 0; k < V; ++k)
+      for (int m = 0; m < M; ++m) {
+        mc[m] = nc[m];
 #pragma unroll
-      for (int f = 0; f < F; ++f) acc[k][f] = zero_v<T>();
-
-    for (int base = head; base < tail; base += TILE) {
-      int nc[M];
-      float nv[M][V];
-      const bool more = base + TILE < tail;
-      bool loaded = false;
-      if (more) {
-        load_tile<V, M, G>(a, base + TILE, tail, l, pol_a, nc, nv);
-        loaded = true;
-      } else if (h1 < t1) {  // first tile of the next unit
-        load_tile<V, M, G>(a, h1, t1, l, pol_a, nc, nv);
-        loaded = true;
-        have = true;
-      }
-      const int cnt = tail - base;
-      if (cnt >= TILE)
-        mac_tile<V, F, G, M, U, VEC, true>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
-      else
-        mac_tile<V, F, G, M, U, VEC, false>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
-      if (loaded) {
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          mc[m] = nc[m];
-#pragma unroll
-          for (int k = 0; k < V; ++k) mv[m][k] = nv[m][k];
-        }
+        for (int k = 0; k < V; ++k) mv[m][k] = nv[m][k];
       }
     }
+  }
 
-    if (S == 0) {
+  if (unit >= a.units) return;
+  if (S == 0) {
 #pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const int64_t row = u * V + k;
-        if (row < a.n_rows) {
-          T *crow = reinterpret_cast<T *>(a.C + row * a.ldc);
+    for (int k = 0; k < V; ++k) {
+      const int64_t row = unit * V + k;
+      if (row < a.n_rows) {
+        T *crow = reinterpret_cast<T *>(a.C + row * a.ldc);
 #pragma unroll
-          for (int f = 0; f < F; ++f)
-            if (cok[f]) st_c(crow + coff[f] / VW, acc[k][f]);
-        }
-      }
-    } else {
-      const int panel = a.trow[u];
-      const bool sole = (u == 0 || a.trow[u - 1] != panel) &&
-                        (u + 1 == a.units || a.trow[u + 1] != panel);
-#pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const int64_t row = (int64_t)panel * V + k;
-        if (row < a.n_rows) {
-          T *crow = reinterpret_cast<T *>(a.C + row * a.ldc);
-#pragma unroll
-          for (int f = 0; f < F; ++f)
-            if (cok[f]) {
-              if (sole)
-                st_c(crow + coff[f] / VW, acc[k][f]);
-              else
-                red_c(crow + coff[f] / VW, acc[k][f]);
-            }
-        }
+        for (int f = 0; f < F; ++f)
+          if (cok[f]) st_c(crow + coff[f] / VW, acc[k][f]);
       }
     }
-    u = u1;
-    head = h1;
-    tail = t1;
-    u1 = u2;
-    h1 = h2;
-    t1 = t2;
+  } else {
+    const int panel = a.trow[unit];
+    const bool sole = (unit == 0 || a.trow[unit - 1] != panel) &&
+                      (unit + 1 == a.units_total || a.trow[unit + 1] != panel);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int64_t row = (int64_t)panel * V + k;
+      if (row < a.n_rows) {
+        T *crow = reinterpret_cast<T *>(a.C + row * a.ldc);
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+          if (cok[f]) {
+            if (sole)
+              st_c(crow + coff[f] / VW, acc[k][f]);
+            else
+              red_c(crow + coff[f] / VW, acc[k][f]);
+          }
+      }
+    }
   }
 }
 

@@ -36,7 +36,7 @@ struct TmaArgs {
   const int32_t *__restrict__ trow;
   float *__restrict__ C;
   int64_t ldc;
-  int32_t n_rows, units, K;
+  int32_t n_rows, unit_begin, units, units_total, K;  // units = end of this launch's range
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256, 1) spmm_tma_kernel(const __grid_constant_
   const int rsub = lane / KP % R;        // which of the R rows of an LDS step
   const int q = KP >= 32 ? lane : lane % KP;  // float4 column (first of FQ)
   const int c0 = blockIdx.y * 4 * KP;    // first float column of this pass
-  const int64_t unit = (int64_t)blockIdx.x * nwarps + warp;
+  const int64_t unit = a.unit_begin + (int64_t)blockIdx.x * nwarps + warp;
   if (unit >= a.units) return;
   const int head = a.rowptr[unit], tail = a.rowptr[unit + 1];
   const int nvec = tail - head;
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256, 1) spmm_tma_kernel(const __grid_constant_
   } else {
     prow = a.trow[unit];
     sole = (unit == 0 || a.trow[unit - 1] != prow) &&
-           (unit + 1 == a.units || a.trow[unit + 1] != prow);
+           (unit + 1 == a.units_total || a.trow[unit + 1] != prow);
   }
 #pragma unroll
   for (int k = 0; k < V; ++k) {
@@ -264,7 +264,8 @@ bool tma_supported(int32_t K, int64_t ldb, int64_t ldc, const float *d_B, const 
 
 // Mode 2 dispatch (called from run_spmm after validation and the S = 1 zeroing).
 pspmm_status run_spmm_tma(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
-                          float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream) {
+                          float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
+                          int64_t u0, int64_t u1) {
   if (!tma_supported(K, ldb, ldc, d_B, d_C))
     PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run mode 2: unsupported K / layout");
   const int KP = tma_kp(K);
@@ -296,9 +297,12 @@ pspmm_status run_spmm_tma(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, 
   args.C = d_C;
   args.ldc = ldc;
   args.n_rows = (int32_t)A->n_rows;
-  args.units = (int32_t)A->num_chunks;
+  args.unit_begin = (int32_t)u0;
+  args.units = (int32_t)u1;
+  args.units_total = (int32_t)A->num_chunks;
   args.K = K;
-  const int64_t bx = (A->num_chunks + warps - 1) / warps;
+  if (u1 <= u0) return PSPMM_OK;
+  const int64_t bx = (u1 - u0 + warps - 1) / warps;
   fn<<<dim3((unsigned)bx, (unsigned)passes), warps * 32, smem, stream>>>(map, args);
   PSPMM_CUDA_TRY(cudaGetLastError());
   return PSPMM_OK;

@@ -238,21 +238,25 @@ def test_config_errors():
     assert st == api.PSPMM_ERR_DIM_MISMATCH  # K < 1
 
 
-def test_host_e2e_entry():
+@pytest.mark.parametrize("V,S", [(1, 0), (1, 1), (2, 0), (2, 1)])
+@pytest.mark.parametrize("mode", [0, 2])
+def test_host_e2e_entry(V, S, mode):
+    """Host entry: H2D, engine in 8 panel-aligned slices, overlapped D2H."""
     api, torch = _api(), _torch()
     g = graph("products_s")
     K = 128
     B = gen.dense(g.n, K, 81)
     ref, mag = oracle_ref(g, B, key=("products_s", K, "e2e"))
     rp, ci, vl = dev(g)
-    cfg = api.Config(V=1, S=1, F=1)
-    A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, 1, 1)
+    cfg = api.Config(V=V, S=S, F=1, mode=mode, sg_override=0)
+    A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, V, S, 32, 16 if S else 0)  # many splits
     hB = torch.from_numpy(B).pin_memory()
-    hC = torch.empty((g.n, K)).pin_memory()
+    hC = torch.full((g.n, K), float("nan")).pin_memory()
     dB = torch.empty((g.n, K), device="cuda")
     dC = torch.empty((g.n, K), device="cuda")
-    api.pspmm_spmm_run_host(A, hB, hC, cfg, dB, dC)
-    assert_parity(hC.numpy(), ref, mag, "host e2e")
+    for _ in range(2):  # second call reuses the handle's copy stream
+        api.pspmm_spmm_run_host(A, hB, hC, cfg, dB, dC)
+        assert_parity(hC.numpy(), ref, mag, f"host e2e V{V} S{S} mode{mode}")
 
 
 def test_graph_capture_and_streams():

@@ -60,7 +60,7 @@ def corpus_graphs(count, seed=12345):
             g = gen.community(n, int(rng.choice([32, 128, 512, 2048])), float(rng.uniform(4, 64)),
                               float(rng.uniform(0.5, 0.95)), s, ordered=(kind == "community"))
         else:
-            d = float(rng.uniform(4, 200))
+            d = float(min(rng.uniform(4, 200), 2e7 / n))  # keep nnz <= 2e7 (sweep time)
             nnz = int(n * d) // 2 * 2
             rp, ci = gen.chung_lu(n, nnz, int(min(n - 1, d * rng.uniform(10, 60))), s,
                                   shuffle_seed=s + 1)
