@@ -198,6 +198,20 @@ pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, in
                                  float *d_Cbuf, void *stream);
 
 /*
+ * (f3) CSR of A^T on the device, for the backward SpMM of a GNN layer
+ * (dL/dB = A^T . dL/dC).  A is n_rows x n_cols
+ * canonical CSR; the outputs are caller-allocated device arrays:
+ * d_t_rowptr[n_cols + 1], d_t_colidx[nnz], d_t_val[nnz].  Rows of A^T hold
+ * A's row indices in ascending order (a stable sort by column), so the
+ * result is canonical and deterministic.  Validates A first; synchronises
+ * `stream`.
+ */
+pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                 const int32_t *d_rowptr, const int32_t *d_colidx,
+                                 const float *d_val, int32_t *d_t_rowptr, int32_t *d_t_colidx,
+                                 float *d_t_val, void *stream);
+
+/*
  * (a2) Table 3 features of a CSR matrix on the device.  Degree
  * and bandwidth statistics are exact integer reductions; SR_1, SR_2, PR_1,
  * PR_2 use the PCSR counting kernels with the given omega.  Synchronises

@@ -105,6 +105,7 @@ _sig("pspmm_pcsr_destroy", None, _P)
 _sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
 _sig("pspmm_features_compute", _st, _i64, _i64, _P, _P, _i32, _P, ctypes.POINTER(Features))
+_sig("pspmm_csr_transpose", _st, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P)
 _sig("pspmm_decide_config", _st, ctypes.POINTER(Features), _i32, ctypes.POINTER(Config))
 _sig("pspmm_shard_plan", _st, _i64, _P, _i32, _i32, _P)
 _sig("pspmm_shard_extract", _st, _i64, _P, _P, _P, _i32, _P, _i32, _P, _P, _P,
@@ -276,6 +277,22 @@ def pspmm_features_compute(n, nnz, rowptr, colidx, omega=32, stream=None) -> dic
                                      ctypes.byref(f))
     _check(st, "pspmm_features_compute")
     return f.as_dict()
+
+
+def pspmm_csr_transpose(n_rows, n_cols, rowptr, colidx, val, stream=None):
+    """CSR of A^T (device tensors in, new device tensors out)."""
+    torch = _torch()
+    nnz = int(rowptr[-1].item())
+    t_rp = torch.empty(n_cols + 1, dtype=torch.int32, device=rowptr.device)
+    t_ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=rowptr.device)
+    t_vl = torch.empty(max(nnz, 1), dtype=torch.float32, device=rowptr.device)
+    st = _lib.pspmm_csr_transpose(n_rows, n_cols, nnz, _dev(rowptr, torch.int32, "rowptr"),
+                                  _dev(colidx, torch.int32, "colidx"),
+                                  _dev(val, torch.float32, "val"), _dev(t_rp, torch.int32, "t"),
+                                  _dev(t_ci, torch.int32, "t"), _dev(t_vl, torch.float32, "t"),
+                                  _stream(stream))
+    _check(st, "pspmm_csr_transpose")
+    return t_rp, t_ci[:nnz], t_vl[:nnz]
 
 
 def pspmm_decide_config(features: dict, K: int) -> Config:

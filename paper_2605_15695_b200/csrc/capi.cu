@@ -161,6 +161,14 @@ pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, in
   return run_spmm_host(A, h_B, ldb, K, h_C, ldc, cfg, d_Bbuf, d_Cbuf, as_stream(stream));
 }
 
+pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                 const int32_t *d_rowptr, const int32_t *d_colidx,
+                                 const float *d_val, int32_t *d_t_rowptr, int32_t *d_t_colidx,
+                                 float *d_t_val, void *stream) {
+  return csr_transpose(n_rows, n_cols, nnz, d_rowptr, d_colidx, d_val, d_t_rowptr, d_t_colidx,
+                       d_t_val, as_stream(stream));
+}
+
 pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                                     const int32_t *d_colidx, int32_t omega, void *stream,
                                     pspmm_features *out) {

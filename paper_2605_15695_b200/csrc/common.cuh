@@ -89,6 +89,11 @@ pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32
                            int64_t ldc, const pspmm_config &cfg, float *d_Bbuf, float *d_Cbuf,
                            cudaStream_t stream);
 
+// transpose.cu (f3: backward SpMM operand)
+pspmm_status csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t *d_rowptr,
+                           const int32_t *d_colidx, const float *d_val, int32_t *d_t_rowptr,
+                           int32_t *d_t_colidx, float *d_t_val, cudaStream_t stream);
+
 // features.cu
 pspmm_status compute_features(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                               const int32_t *d_colidx, int32_t omega, cudaStream_t stream,

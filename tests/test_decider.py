@@ -1,0 +1,102 @@
+"""(a3) The compiled decider: the C function evaluates exactly the tree that
+tools/train_decider.py emitted into csrc/decider_model.h (re-walked here in
+Python from the header's arrays), and the trainer's cost-sensitive CART
+recovers a planted rule.  Parity of C is independent of the config (c-4:
+"parity unpinned" for the decider itself); these tests pin the plumbing."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "paper_2605_15695_b200", "csrc", "decider_model.h")
+FEATS = ("n", "n_hat", "nnz", "delta", "d", "d_hat", "d_max", "cv", "cv_hat", "sr1", "sr2", "rho",
+         "b", "b_max", "pr1", "pr2")
+
+
+def parse_header():
+    text = open(HEADER).read()
+    trained = "#define PSPMM_DECIDER_TRAINED 1" in text
+
+    def arr(name, conv):
+        m = re.search(name + r"\[kNodes\](?:\[\d\])? = \{(.*?)\};", text, re.S)
+        return m.group(1)
+
+    feat = [int(x) for x in arr("kFeature", int).split(",")]
+    thr = [float(x) for x in arr("kThreshold", float).split(",")]
+    left = [int(x) for x in arr("kLeft", int).split(",")]
+    right = [int(x) for x in arr("kRight", int).split(",")]
+    labs = [tuple(int(y) for y in g.split(",")) for g in re.findall(r"\{([-\d, ]+)\}",
+                                                                     arr("kLabel", str))]
+    return trained, feat, thr, left, right, labs
+
+
+def walk(model, f, K):
+    _, feat, thr, left, right, labs = model
+    node = 0
+    x = [f[k] for k in FEATS] + [math.log2(K)]
+    while feat[node] >= 0:
+        node = left[node] if x[feat[node]] <= thr[node] else right[node]
+    return labs[node]
+
+
+def ceil_pow2(x):
+    p = 1
+    while p < x and p < 32:
+        p <<= 1
+    return p
+
+
+def test_c_decider_evaluates_the_header_tree():
+    from paper_2605_15695_b200 import api
+    model = parse_header()
+    if not model[0]:
+        pytest.skip("decider not trained yet (rule mode)")
+    rng = np.random.default_rng(0)
+    for _ in range(400):
+        n = float(rng.integers(1000, 3_000_000))
+        d = float(rng.uniform(1, 600))
+        f = dict(n=n, n_hat=n * rng.uniform(0.5, 1), nnz=n * d, delta=rng.uniform(0.5, 1), d=d,
+                 d_hat=d * rng.uniform(1, 2), d_max=d * rng.uniform(1, 100),
+                 cv=rng.uniform(0, 5), cv_hat=rng.uniform(0, 5), sr1=rng.uniform(1, 2),
+                 sr2=rng.uniform(1, 2), rho=d / n, b=rng.uniform(0, n), b_max=n - 1, pr1=0.0,
+                 pr2=rng.uniform(0, 0.5))
+        K = int(rng.choice([8, 16, 32, 48, 64, 96, 128, 160, 256]))
+        mode, V, S, W, F, P = walk(model, f, K)
+        c = api.pspmm_decide_config(f, K)
+        if mode == 2 and K % 32 == 0:
+            assert (c.mode, c.V, c.S, c.W) == (2, V, S, W)
+        else:
+            assert (c.mode, c.V, c.S, c.W) == (0, V, S, W)
+            if mode == 0:
+                q = (K + 3) // 4
+                assert c.F == F and c.G == ceil_pow2(-(-q // (F * P)))
+
+
+def test_trainer_recovers_planted_rule():
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import train_decider as td
+    rng = np.random.default_rng(1)
+    recs = []
+    for i in range(120):
+        f = {k: float(rng.uniform(0, 1)) for k in FEATS}
+        f["d_max"] = float(rng.uniform(0, 100))
+        K = 64
+        # planted: S = 1 is 2x faster iff d_max > 50, V = 2 iff pr2 < 0.3
+        table = []
+        for V in (1, 2):
+            for S in (0, 1):
+                ms = 1.0
+                ms *= 0.5 if (S == 1) == (f["d_max"] > 50) else 1.0
+                ms *= 0.7 if (V == 2) == (f["pr2"] < 0.3) else 1.0
+                table.append({"V": V, "S": S, "W": 2, "F": 1, "G": 16, "mode": 0, "ms": ms})
+        recs.append({"graph": f"g{i}", "K": K, "features": f, "table": table,
+                     "decided": {"F": 1, "G": 16}})
+    keys, X, perf = td.build_matrix(recs)
+    root = td.fit(X, perf, 4, 3)
+    ev = td.evaluate(recs, keys, X, perf, list(range(len(recs))), root)
+    assert ev["pre"] > 0.99 and ev["rnd"] < 0.8

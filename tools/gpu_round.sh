@@ -37,10 +37,10 @@ if want ncu; then
 fi
 if want sweep; then
   timeout 1800 python tools/sweep.py --workloads cora,roadnet,reddit,proteins,products --iters 5 \
-      --out $O/sweep_workloads.json > $O/sweep_workloads.log 2>&1
+      --modes 0,2 --Ws 2,4,8 --out $O/sweep_workloads.json > $O/sweep_workloads.log 2>&1
 fi
 if want corpus; then
-  timeout 2400 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 \
+  timeout 3000 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --Ws 2,4 --modes 0,2 \
       --out $O/sweep_corpus.json > $O/sweep_corpus.log 2>&1
 fi
 # never let gpurun_out/ exceed the 64 MiB merge limit
