@@ -64,13 +64,22 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
   c.sg_override = 0;
   c.mode = 0;
 #if PSPMM_DECIDER_TRAINED
-  int node = 0;
-  while (pspmm_model::kFeature[node] >= 0) {
-    const double x = feature_value(f, pspmm_model::kFeature[node], K);
-    node = x <= pspmm_model::kThreshold[node] ? pspmm_model::kLeft[node]
-                                              : pspmm_model::kRight[node];
+  // random forest: every tree votes for its leaf's label; the label
+  // with the most votes wins, ties to the lowest label id
+  int votes[pspmm_model::kNumLabels] = {};
+  for (int t = 0; t < pspmm_model::kTrees; ++t) {
+    int node = pspmm_model::kRoot[t];
+    while (pspmm_model::kFeature[node] >= 0) {
+      const double x = feature_value(f, pspmm_model::kFeature[node], K);
+      node = x <= pspmm_model::kThreshold[node] ? pspmm_model::kLeft[node]
+                                                : pspmm_model::kRight[node];
+    }
+    votes[pspmm_model::kLeafLabel[node]]++;
   }
-  const int *lab = pspmm_model::kLabel[node];
+  int best = 0;
+  for (int l = 1; l < pspmm_model::kNumLabels; ++l)
+    if (votes[l] > votes[best]) best = l;
+  const int *lab = pspmm_model::kLabel[best];
   c.mode = lab[0];
   c.V = lab[1];
   c.S = lab[2];

@@ -21,26 +21,31 @@ def parse_header():
     text = open(HEADER).read()
     trained = "#define PSPMM_DECIDER_TRAINED 1" in text
 
-    def arr(name, conv):
-        m = re.search(name + r"\[kNodes\](?:\[\d\])? = \{(.*?)\};", text, re.S)
+    def arr(name):
+        m = re.search(r"\b" + name + r"\[\w+\](?:\[\d\])? = \{(.*)\};", text)
         return m.group(1)
 
-    feat = [int(x) for x in arr("kFeature", int).split(",")]
-    thr = [float(x) for x in arr("kThreshold", float).split(",")]
-    left = [int(x) for x in arr("kLeft", int).split(",")]
-    right = [int(x) for x in arr("kRight", int).split(",")]
+    roots = [int(x) for x in arr("kRoot").split(",")]
+    feat = [int(x) for x in arr("kFeature").split(",")]
+    thr = [float(x) for x in arr("kThreshold").split(",")]
+    left = [int(x) for x in arr("kLeft").split(",")]
+    right = [int(x) for x in arr("kRight").split(",")]
+    leaf = [int(x) for x in arr("kLeafLabel").split(",")]
     labs = [tuple(int(y) for y in g.split(",")) for g in re.findall(r"\{([-\d, ]+)\}",
-                                                                     arr("kLabel", str))]
-    return trained, feat, thr, left, right, labs
+                                                                     arr("kLabel"))]
+    return trained, roots, feat, thr, left, right, leaf, labs
 
 
 def walk(model, f, K):
-    _, feat, thr, left, right, labs = model
-    node = 0
+    """Majority vote of the forest, ties to the lowest label id."""
+    _, roots, feat, thr, left, right, leaf, labs = model
     x = [f[k] for k in FEATS] + [math.log2(K)]
-    while feat[node] >= 0:
-        node = left[node] if x[feat[node]] <= thr[node] else right[node]
-    return labs[node]
+    votes = [0] * len(labs)
+    for node in roots:
+        while feat[node] >= 0:
+            node = left[node] if x[feat[node]] <= thr[node] else right[node]
+        votes[leaf[node]] += 1
+    return labs[votes.index(max(votes))]
 
 
 def ceil_pow2(x):

@@ -86,7 +86,9 @@ class Node:
         self.label, self.feat, self.thr, self.left, self.right = label, feat, thr, left, right
 
 
-def fit(X, perf, depth, min_leaf):
+def fit(X, perf, depth, min_leaf, rng=None, mtry=None):
+    """Cost-sensitive CART.  With rng, each split draws `mtry` candidate
+    features (random-forest trees)."""
     score = perf.sum(0)
     label = int(np.argmax(score))
     node = Node(label=label)
@@ -94,7 +96,10 @@ def fit(X, perf, depth, min_leaf):
         return node
     base = score[label]
     best = (base + 1e-9, None, None)
-    for f in range(X.shape[1]):
+    feats = range(X.shape[1])
+    if rng is not None:
+        feats = rng.choice(X.shape[1], size=mtry or int(math.sqrt(X.shape[1])) + 1, replace=False)
+    for f in feats:
         order = np.argsort(X[:, f], kind="stable")
         xs = X[order, f]
         cum = np.cumsum(perf[order], 0)
@@ -110,15 +115,33 @@ def fit(X, perf, depth, min_leaf):
     f, thr = best[1], best[2]
     m = X[:, f] <= thr
     node.feat, node.thr = f, thr
-    node.left = fit(X[m], perf[m], depth - 1, min_leaf)
-    node.right = fit(X[~m], perf[~m], depth - 1, min_leaf)
+    node.left = fit(X[m], perf[m], depth - 1, min_leaf, rng, mtry)
+    node.right = fit(X[~m], perf[~m], depth - 1, min_leaf, rng, mtry)
     return node
 
 
-def predict(node, x):
-    while node.feat >= 0:
-        node = node.left if x[node.feat] <= node.thr else node.right
-    return node.label
+def fit_forest(X, perf, trees, depth, min_leaf, seed=2605):
+    """Random forest of cost-sensitive trees: bootstrap records,
+    random feature subsets per split; prediction = majority vote."""
+    if trees <= 1:
+        return [fit(X, perf, depth, min_leaf)]
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(trees):
+        idx = rng.integers(0, len(X), len(X))
+        out.append(fit(X[idx], perf[idx], depth, min_leaf, rng))
+    return out
+
+
+def predict(model, x):
+    roots = model if isinstance(model, list) else [model]
+    votes = {}
+    for node in roots:
+        while node.feat >= 0:
+            node = node.left if x[node.feat] <= node.thr else node.right
+        votes[node.label] = votes.get(node.label, 0) + 1
+    best = max(votes.values())
+    return min(k for k, v in votes.items() if v == best)  # ties -> lowest label id
 
 
 def flatten(root):
@@ -158,27 +181,40 @@ def evaluate(recs, keys, X, perf, test_idx, root, seed=0):
             "rule": float(np.nanmean(rule)) if rule else None, "n_test": len(test_idx)}
 
 
-def emit_header(path, keys, root, source):
-    nodes = flatten(root)
-    lines = ["// Decision-tree model of the SpMM-decider (DESIGN.md §6).",
-             f"// GENERATED by tools/train_decider.py from {source}; do not edit.",
+def emit_header(path, keys, model, source):
+    """Forest -> csrc/decider_model.h: concatenated node arrays, per-tree roots,
+    per-node label ids into a table of distinct labels."""
+    roots = model if isinstance(model, list) else [model]
+    nodes, root_idx = [], []
+    for r in roots:
+        base = len(nodes)
+        ns = flatten(r)
+        root_idx.append(base)
+        for n in ns:
+            n._gl = base + getattr(n, "_l", -1 - base) if n.feat >= 0 else -1
+            n._gr = base + getattr(n, "_r", -1 - base) if n.feat >= 0 else -1
+        nodes += ns
+    used = sorted({n.label for n in nodes if n.feat < 0})
+    lid = {k: i for i, k in enumerate(used)}
+    lines = ["// Random-forest model of the SpMM-decider (DESIGN.md section 6).",
+             f"// GENERATED by tools/train_decider.py from {os.path.basename(source)}; do not edit.",
              "#pragma once", "#define PSPMM_DECIDER_TRAINED 1",
              f'#define PSPMM_DECIDER_SOURCE "{os.path.basename(source)}"',
-             "namespace pspmm_model {", f"constexpr int kNodes = {len(nodes)};",
+             "namespace pspmm_model {", f"constexpr int kTrees = {len(roots)};",
+             f"constexpr int kNodes = {len(nodes)};", f"constexpr int kNumLabels = {len(used)};",
              "// feature index: 0..15 = pspmm_features fields in header order, 16 = log2(K)"]
-    feat = [n.feat for n in nodes]
-    thr = [n.thr for n in nodes]
-    left = [getattr(n, "_l", -1) for n in nodes]
-    right = [getattr(n, "_r", -1) for n in nodes]
-    lab = [keys[n.label] if n.label is not None else (0, 1, 0, 4, 1, 1) for n in nodes]
-    lines.append("constexpr int kFeature[kNodes] = {" + ", ".join(map(str, feat)) + "};")
+    lines.append("constexpr int kRoot[kTrees] = {" + ", ".join(map(str, root_idx)) + "};")
+    lines.append("constexpr int kFeature[kNodes] = {" + ", ".join(str(n.feat) for n in nodes) + "};")
     lines.append("constexpr double kThreshold[kNodes] = {" +
-                 ", ".join(repr(float(t)) for t in thr) + "};")
-    lines.append("constexpr int kLeft[kNodes] = {" + ", ".join(map(str, left)) + "};")
-    lines.append("constexpr int kRight[kNodes] = {" + ", ".join(map(str, right)) + "};")
-    lines.append("// leaf label: {mode, V, S, W, F, P (column passes)}")
-    lines.append("constexpr int kLabel[kNodes][6] = {" +
-                 ", ".join("{" + ", ".join(map(str, l)) + "}" for l in lab) + "};")
+                 ", ".join(repr(float(n.thr)) for n in nodes) + "};")
+    lines.append("constexpr int kLeft[kNodes] = {" + ", ".join(str(n._gl) for n in nodes) + "};")
+    lines.append("constexpr int kRight[kNodes] = {" + ", ".join(str(n._gr) for n in nodes) + "};")
+    lines.append("// leaf -> label id (-1 for inner nodes)")
+    lines.append("constexpr int kLeafLabel[kNodes] = {" +
+                 ", ".join(str(lid[n.label]) if n.feat < 0 else "-1" for n in nodes) + "};")
+    lines.append("// label: {mode, V, S, W, F, P (column passes)}")
+    lines.append("constexpr int kLabel[kNumLabels][6] = {" +
+                 ", ".join("{" + ", ".join(map(str, keys[k])) + "}" for k in used) + "};")
     lines.append("}  // namespace pspmm_model")
     open(path, "w").write("\n".join(lines) + "\n")
 
@@ -188,6 +224,7 @@ def main():
     ap.add_argument("inputs", nargs="+")
     ap.add_argument("--depth", type=int, default=6)
     ap.add_argument("--min-leaf", type=int, default=3)
+    ap.add_argument("--trees", type=int, default=32, help="forest size (1 = a single CART tree)")
     ap.add_argument("--out-header", default=os.path.join(ROOT, "paper_2605_15695_b200", "csrc",
                                                          "decider_model.h"))
     ap.add_argument("--eval-json", default=None)
@@ -199,20 +236,24 @@ def main():
     test_graphs = set(rng.choice(graphs, size=max(1, len(graphs) // 5), replace=False).tolist())
     tr = [i for i, r in enumerate(recs) if r["graph"] not in test_graphs]
     te = [i for i, r in enumerate(recs) if r["graph"] in test_graphs]
-    root = fit(X[tr], perf[tr], a.depth, a.min_leaf)
-    ev = evaluate(recs, keys, X, perf, te, root)
-    ev_train = evaluate(recs, keys, X, perf, tr, root)
-    per_k = {}
-    for K in sorted({r["K"] for r in recs}):
-        idx = [i for i in te if recs[i]["K"] == K]
-        if idx:
-            per_k[K] = evaluate(recs, keys, X, perf, idx, root)
     report = {"records": len(recs), "graphs": len(graphs), "labels": len(keys),
-              "held_out": ev, "train": ev_train, "held_out_per_K": per_k,
-              "protocol": "80/20 split by graph (P:399); normalized performance = t_best / t"}
-    # final model on all records
-    root_all = fit(X, perf, a.depth, a.min_leaf)
-    emit_header(a.out_header, keys, root_all, ",".join(a.inputs))
+              "test_graphs": sorted(test_graphs),
+              "protocol": "80/20 split by graph (P:399); normalized performance = t_best / t; "
+                          "rnd = a uniformly random valid lattice config; rule = the untrained "
+                          "decide.cpp rule"}
+    for name, trees in (("tree", 1), ("forest", a.trees)):
+        model = fit_forest(X[tr], perf[tr], trees, a.depth, a.min_leaf)
+        per_k = {}
+        for K in sorted({r["K"] for r in recs}):
+            idx = [i for i in te if recs[i]["K"] == K]
+            if idx:
+                per_k[K] = evaluate(recs, keys, X, perf, idx, model)
+        report[name] = {"held_out": evaluate(recs, keys, X, perf, te, model),
+                        "train": evaluate(recs, keys, X, perf, tr, model),
+                        "held_out_per_K": per_k}
+    # the shipped model: the forest, refit on all records
+    model = fit_forest(X, perf, a.trees, a.depth, a.min_leaf)
+    emit_header(a.out_header, keys, model, ",".join(a.inputs))
     print(json.dumps(report, indent=1))
     if a.eval_json:
         json.dump(report, open(a.eval_json, "w"), indent=1)
