@@ -212,6 +212,39 @@ pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,
                                  float *d_t_val, void *stream);
 
 /*
+ * (f1) Locality reordering (§4.4; Rabbit itself is not
+ * reimplemented).  Host function over host CSR arrays; writes
+ * perm[old] = new for all n nodes (a bijection).  strategy 0 = identity,
+ * 1 = BFS / Cuthill-McKee (components by descending size, pseudo-peripheral
+ * start, neighbours by ascending degree; the pattern is symmetrised),
+ * 2 = descending degree (stable).  Deterministic.
+ */
+pspmm_status pspmm_reorder(int64_t n, const int32_t *h_rowptr, const int32_t *h_colidx,
+                           int32_t strategy, int32_t *h_perm);
+
+/*
+ * (f1) A' = P A P^T on the device: row i of A becomes row perm[i], column j
+ * becomes perm[j], columns re-sorted ascending per row (canonical).  d_perm
+ * is a device int32 bijection of [0, n).  Outputs are caller-allocated:
+ * d_out_rowptr[n + 1], d_out_colidx[nnz], d_out_val[nnz].  Validates A;
+ * synchronises `stream`.
+ */
+pspmm_status pspmm_csr_permute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                               const int32_t *d_colidx, const float *d_val, const int32_t *d_perm,
+                               int32_t *d_out_rowptr, int32_t *d_out_colidx, float *d_out_val,
+                               void *stream);
+
+/*
+ * (f1) Row permutation of a dense n x K fp32 matrix on the device:
+ * inverse == 0: out[perm[i]] = in[i]   (B' = P B before the SpMM)
+ * inverse != 0: out[i] = in[perm[i]]   (C = P^T C' after it)
+ * in and out must not alias.  Asynchronous on `stream`.
+ */
+pspmm_status pspmm_permute_rows(int64_t n, int32_t K, const float *d_in, int64_t ldi,
+                                const int32_t *d_perm, float *d_out, int64_t ldo, int32_t inverse,
+                                void *stream);
+
+/*
  * (a2) Table 3 features of a CSR matrix on the device.  Degree
  * and bandwidth statistics are exact integer reductions; SR_1, SR_2, PR_1,
  * PR_2 use the PCSR counting kernels with the given omega.  Synchronises

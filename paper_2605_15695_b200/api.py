@@ -106,6 +106,9 @@ _sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
 _sig("pspmm_features_compute", _st, _i64, _i64, _P, _P, _i32, _P, ctypes.POINTER(Features))
 _sig("pspmm_csr_transpose", _st, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P)
+_sig("pspmm_reorder", _st, _i64, _P, _P, _i32, _P)
+_sig("pspmm_csr_permute", _st, _i64, _i64, _P, _P, _P, _P, _P, _P, _P, _P)
+_sig("pspmm_permute_rows", _st, _i64, _i32, _P, _i64, _P, _P, _i64, _i32, _P)
 _sig("pspmm_decide_config", _st, ctypes.POINTER(Features), _i32, ctypes.POINTER(Config))
 _sig("pspmm_shard_plan", _st, _i64, _P, _i32, _i32, _P)
 _sig("pspmm_shard_extract", _st, _i64, _P, _P, _P, _i32, _P, _i32, _P, _P, _P,
@@ -293,6 +296,51 @@ def pspmm_csr_transpose(n_rows, n_cols, rowptr, colidx, val, stream=None):
                                   _stream(stream))
     _check(st, "pspmm_csr_transpose")
     return t_rp, t_ci[:nnz], t_vl[:nnz]
+
+
+REORDER = {"identity": 0, "bfs": 1, "degree": 2}
+
+
+def pspmm_reorder(rowptr, colidx, strategy="bfs") -> np.ndarray:
+    """perm[old] = new (host numpy int32) — P:271-272 reordering stand-in."""
+    rp, prp = _host(rowptr, np.int32)
+    ci, pci = _host(colidx, np.int32)
+    n = rp.shape[0] - 1
+    perm = np.empty(n, np.int32)
+    st = _lib.pspmm_reorder(n, prp, pci, REORDER.get(strategy, strategy),
+                            perm.ctypes.data_as(_P))
+    _check(st, "pspmm_reorder")
+    return perm
+
+
+def pspmm_csr_permute(rowptr, colidx, val, perm, stream=None):
+    """A' = P A P^T on the device (torch tensors in and out)."""
+    torch = _torch()
+    n = rowptr.shape[0] - 1
+    nnz = int(rowptr[-1].item())
+    o_rp = torch.empty(n + 1, dtype=torch.int32, device=rowptr.device)
+    o_ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=rowptr.device)
+    o_vl = torch.empty(max(nnz, 1), dtype=torch.float32, device=rowptr.device)
+    st = _lib.pspmm_csr_permute(n, nnz, _dev(rowptr, torch.int32, "rowptr"),
+                                _dev(colidx, torch.int32, "colidx"),
+                                _dev(val, torch.float32, "val"), _dev(perm, torch.int32, "perm"),
+                                _dev(o_rp, torch.int32, "o"), _dev(o_ci, torch.int32, "o"),
+                                _dev(o_vl, torch.float32, "o"), _stream(stream))
+    _check(st, "pspmm_csr_permute")
+    return o_rp, o_ci[:nnz], o_vl[:nnz]
+
+
+def pspmm_permute_rows(X, perm, inverse=False, out=None, stream=None):
+    """inverse=False: out[perm[i]] = X[i]; inverse=True: out[i] = X[perm[i]]."""
+    torch = _torch()
+    x, ldi = _dense(X, "X")
+    if out is None:
+        out = torch.empty_like(X)
+    o, ldo = _dense(out, "out")
+    st = _lib.pspmm_permute_rows(X.shape[0], X.shape[1], x, ldi, _dev(perm, torch.int32, "perm"),
+                                 o, ldo, 1 if inverse else 0, _stream(stream))
+    _check(st, "pspmm_permute_rows")
+    return out
 
 
 def pspmm_decide_config(features: dict, K: int) -> Config:

@@ -169,6 +169,20 @@ pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,
                        d_t_val, as_stream(stream));
 }
 
+pspmm_status pspmm_csr_permute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
+                               const int32_t *d_colidx, const float *d_val, const int32_t *d_perm,
+                               int32_t *d_out_rowptr, int32_t *d_out_colidx, float *d_out_val,
+                               void *stream) {
+  return csr_permute(n, nnz, d_rowptr, d_colidx, d_val, d_perm, d_out_rowptr, d_out_colidx,
+                     d_out_val, as_stream(stream));
+}
+
+pspmm_status pspmm_permute_rows(int64_t n, int32_t K, const float *d_in, int64_t ldi,
+                                const int32_t *d_perm, float *d_out, int64_t ldo, int32_t inverse,
+                                void *stream) {
+  return permute_rows(n, K, d_in, ldi, d_perm, d_out, ldo, inverse, as_stream(stream));
+}
+
 pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                                     const int32_t *d_colidx, int32_t omega, void *stream,
                                     pspmm_features *out) {

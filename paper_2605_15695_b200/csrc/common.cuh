@@ -94,6 +94,14 @@ pspmm_status csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const in
                            const int32_t *d_colidx, const float *d_val, int32_t *d_t_rowptr,
                            int32_t *d_t_colidx, float *d_t_val, cudaStream_t stream);
 
+// permute.cu (f1: applying a reordering)
+pspmm_status csr_permute(int64_t n, int64_t nnz, const int32_t *d_rowptr, const int32_t *d_colidx,
+                         const float *d_val, const int32_t *d_perm, int32_t *d_out_rowptr,
+                         int32_t *d_out_colidx, float *d_out_val, cudaStream_t stream);
+pspmm_status permute_rows(int64_t n, int32_t K, const float *d_in, int64_t ldi,
+                          const int32_t *d_perm, float *d_out, int64_t ldo, int32_t inverse,
+                          cudaStream_t stream);
+
 // features.cu
 pspmm_status compute_features(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                               const int32_t *d_colidx, int32_t omega, cudaStream_t stream,
