@@ -1,0 +1,209 @@
+// (a6, a7) Engine mode 3: short-row pipeline for low-degree graphs
+// (roadNet-like, d ~ 3), V = 1 and S = 0 only.  Same computation as Alg. 2
+// (P:215-267); what changes is the schedule.  The mode-0 engine gives each
+// row group one unit and retires, so every row pays the dependent
+// rowPtr -> colIdx -> B-row -> store latency chain with nothing else in
+// flight.  Here a row group (G lanes, F float4 accumulators per lane) walks
+// rows r, r + stride, ... with a two-deep software pipeline: the rowPtr pair
+// two rows ahead and the (colIdx, val) of the next row (one vector per lane,
+// rows up to G vectors; longer rows fall back to an inner loop) are in flight
+// while the current row's B rows are gathered.  The register footprint stays
+// small (no staged tiles), so more warps are resident.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pspmm {
+namespace {
+
+struct ShortArgs {
+  const int32_t *__restrict__ rowptr;
+  const int32_t *__restrict__ colidx;
+  const float *__restrict__ val;
+  const float *__restrict__ B;
+  float *__restrict__ C;
+  int64_t ldb, ldc;
+  int32_t row_begin, row_end, K;
+};
+
+__device__ __forceinline__ int lda(const int32_t *p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float lda(const float *p) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+template <int F, int G>
+__global__ void __launch_bounds__(256, 4) spmm_short_kernel(const ShortArgs a) {
+  constexpr int UNR = 4;  // vectors of a row whose B rows are in flight together
+  const int lane = threadIdx.x & 31;
+  const int g = lane / G, l = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
+  const int64_t groups = ((int64_t)gridDim.x * blockDim.x >> 5) * (32 / G);
+  const int64_t first = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G) + g;
+  const int col0 = blockIdx.y * G * F * 4;
+  bool cok[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) cok[f] = col0 + (f * G + l) * 4 < a.K;
+  const char *bptr = reinterpret_cast<const char *>(a.B + col0 + l * 4);
+  const uint32_t stride = (uint32_t)(a.ldb * 4);
+
+  int64_t r = a.row_begin + first;
+  // pipeline registers: rowPtr of r and r + groups, the vectors of r
+  int h0 = 0, t0 = 0, h1 = 0, t1 = 0;
+  if (r < a.row_end) {
+    h0 = a.rowptr[r];
+    t0 = a.rowptr[r + 1];
+  }
+  if (r + groups < a.row_end) {
+    h1 = a.rowptr[r + groups];
+    t1 = a.rowptr[r + groups + 1];
+  }
+  int c0 = 0;
+  float v0 = 0.f;
+  if (h0 + l < t0) {
+    c0 = lda(a.colidx + h0 + l);
+    v0 = lda(a.val + h0 + l);
+  }
+  for (; r < a.row_end; r += groups) {
+    // prefetch: rowPtr two rows ahead, vectors of the next row
+    const int64_t r2 = r + 2 * groups;
+    int h2 = 0, t2 = 0;
+    if (r2 < a.row_end) {
+      h2 = a.rowptr[r2];
+      t2 = a.rowptr[r2 + 1];
+    }
+    int c1 = 0;
+    float v1 = 0.f;
+    if (h1 + l < t1) {
+      c1 = lda(a.colidx + h1 + l);
+      v1 = lda(a.val + h1 + l);
+    }
+    float4 acc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int base = h0; base < t0; base += G) {
+      int cb = c0;
+      float vb = v0;
+      if (base != h0) {  // rows longer than G vectors: reload this window
+        cb = base + l < t0 ? lda(a.colidx + base + l) : 0;
+        vb = base + l < t0 ? lda(a.val + base + l) : 0.f;
+      }
+      const int cnt = min(G, t0 - base);
+      for (int j0 = 0; j0 < cnt; j0 += UNR) {
+        float4 b[UNR][F];
+        float vv[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int j = j0 + u;
+          const int c = __shfl_sync(gmask, cb, j & (G - 1), G);
+          vv[u] = __shfl_sync(gmask, vb, j & (G - 1), G);
+          const char *row = bptr + (uint64_t)(uint32_t)c * stride;
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            if (j < cnt && cok[f])
+              b[u][f] = __ldg(reinterpret_cast<const float4 *>(row + f * G * 16));
+            else
+              b[u][f] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            acc[f].x = fmaf(vv[u], b[u][f].x, acc[f].x);
+            acc[f].y = fmaf(vv[u], b[u][f].y, acc[f].y);
+            acc[f].z = fmaf(vv[u], b[u][f].z, acc[f].z);
+            acc[f].w = fmaf(vv[u], b[u][f].w, acc[f].w);
+          }
+      }
+    }
+    float4 *crow = reinterpret_cast<float4 *>(a.C + r * a.ldc + col0 + l * 4);
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+      if (cok[f]) __stcs(crow + f * G, acc[f]);
+    h0 = h1;
+    t0 = t1;
+    h1 = h2;
+    t1 = t2;
+    c0 = c1;
+    v0 = v1;
+  }
+}
+
+using ShortFn = void (*)(const ShortArgs);
+
+template <int F>
+ShortFn pick_g(int G) {
+  switch (G) {
+    case 2: return spmm_short_kernel<F, 2>;
+    case 4: return spmm_short_kernel<F, 4>;
+    case 8: return spmm_short_kernel<F, 8>;
+    case 16: return spmm_short_kernel<F, 16>;
+    case 32: return spmm_short_kernel<F, 32>;
+    default: return nullptr;
+  }
+}
+
+ShortFn pick(int F, int G) {
+  switch (F) {
+    case 1: return pick_g<1>(G);
+    case 2: return pick_g<2>(G);
+    case 4: return pick_g<4>(G);
+    default: return nullptr;
+  }
+}
+
+int ceil_pow2(int x) {
+  int p = 1;
+  while (p < x && p < 32) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+bool short_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc, const float *d_B,
+                     const float *d_C, const pspmm_config &cfg) {
+  return A->V == 1 && A->S == 0 && K % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(d_B) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(d_C) & 15) == 0 &&
+         (cfg.F == 1 || cfg.F == 2 || cfg.F == 4);
+}
+
+pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
+                            float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
+                            int64_t u0, int64_t u1) {
+  if (u1 <= u0) return PSPMM_OK;
+  const int F = cfg.F;
+  int G = cfg.G ? cfg.G : ceil_pow2((K / 4 + F - 1) / F);
+  if (G < 2) G = 2;
+  ShortFn fn = pick(F, G);
+  if (!fn) PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run mode 3: F must be 1, 2 or 4 and G >= 2");
+  ShortArgs args;
+  args.rowptr = A->d_rowptr;
+  args.colidx = A->d_colidx;
+  args.val = A->d_val;
+  args.B = d_B;
+  args.C = d_C;
+  args.ldb = ldb;
+  args.ldc = ldc;
+  args.row_begin = (int32_t)u0;
+  args.row_end = (int32_t)u1;
+  args.K = K;
+  const int threads = std::min(cfg.W, 8) * 32;
+  const int64_t per_block = threads / 32 * (32 / G);
+  // a few waves of resident blocks (256 x 4 launch bounds: 32 warps / SM)
+  const int64_t resident = std::max<int64_t>(1, 1024 / threads);
+  int64_t bx = (u1 - u0 + per_block - 1) / per_block;
+  bx = std::min<int64_t>(bx, (int64_t)num_sms() * resident * 2);
+  const int64_t by = (K + 4 * G * F - 1) / (4 * G * F);
+  fn<<<dim3((unsigned)bx, (unsigned)by), threads, 0, stream>>>(args);
+  PSPMM_CUDA_TRY(cudaGetLastError());
+  return PSPMM_OK;
+}
+
+}  // namespace pspmm

@@ -74,6 +74,8 @@ def test_c_decider_evaluates_the_header_tree():
         c = api.pspmm_decide_config(f, K)
         if mode == 2 and K % 32 == 0:
             assert (c.mode, c.V, c.S, c.W) == (2, V, S, W)
+        elif mode == 3 and K % 4 == 0:
+            assert (c.mode, c.V, c.S, c.W, c.F) == (3, V, S, W, F)
         else:
             assert (c.mode, c.V, c.S, c.W) == (0, V, S, W)
             if mode == 0:

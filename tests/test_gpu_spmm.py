@@ -123,6 +123,31 @@ def test_tma_gather_engine(V, S, K, W):
     assert_parity(C, ref, mag, f"tma V{V} S{S} K{K} W{W}")
 
 
+@pytest.mark.parametrize("name", ["roadnet_s", "cora", "giant", "banded", "reddit_s"])
+@pytest.mark.parametrize("K", [16, 32, 64, 128])
+@pytest.mark.parametrize("F", [1, 2, 4])
+def test_short_row_engine(name, K, F):
+    """Engine mode 3 (V = 1, S = 0): rows of any length (long rows take the
+    inner window loop), every (F, G) the dispatcher can pick."""
+    api = _api()
+    g = graph(name)
+    B = gen.dense(g.n, K, 500 + K)
+    ref, mag = oracle_ref(g, B, key=(name, K, "short"))
+    for W in (2, 8):
+        C, _ = run(g, B, api.Config(W=W, F=F, V=1, S=0, mode=3))
+        assert_parity(C, ref, mag, f"short {name} K{K} F{F} W{W}")
+
+
+def test_short_row_engine_rejects_other_corners():
+    api = _api()
+    g = graph("cora")
+    B = gen.dense(g.n, 16, 1)
+    for V, S in ((2, 0), (1, 1)):
+        with pytest.raises(api.PspmmError) as e:
+            run(g, B, api.Config(V=V, S=S, mode=3))
+        assert e.value.status == api.PSPMM_ERR_UNSUPPORTED
+
+
 def test_tma_engine_rejects_unsupported_K():
     api = _api()
     g = graph("cora")

@@ -41,10 +41,17 @@ def derived_G(K, F, P):
 
 
 def load(paths):
-    recs = []
+    """Sweep records; records of the same (graph, K) from several files
+    (e.g. a later sweep of another engine mode) are merged into one table."""
+    by_key = {}
     for p in paths:
-        recs += json.load(open(p))
-    return recs
+        for r in json.load(open(p)):
+            k = (r["graph"], r["K"])
+            if k in by_key:
+                by_key[k]["table"] = by_key[k]["table"] + r["table"]
+            else:
+                by_key[k] = dict(r)
+    return list(by_key.values())
 
 
 def label_of(K, t):
@@ -56,7 +63,7 @@ def label_of(K, t):
     P = passes_of(K, t["F"], t["G"])
     if derived_G(K, t["F"], P) != t["G"]:
         return None
-    return (0, t["V"], t["S"], t["W"], t["F"], P)
+    return (mode, t["V"], t["S"], t["W"], t["F"], P)
 
 
 def build_matrix(recs):
