@@ -325,6 +325,9 @@ def main():
     ap.add_argument("--headline-only", action="store_true",
                     help="skip the per-config table of the other four workloads")
     ap.add_argument("--no-cusparse", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="N>1: all-gather then SpMM, instead of overlapping the all-gather "
+                         "with the own-column block")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to rehearse the N>1 flow on one GPU")
     args = ap.parse_args()
@@ -397,7 +400,10 @@ def main():
                            f"{world}-way nnz-balanced row shards + NCCL all-gather of B",
             "l2": "flushed between timed steps (256 MiB write, untimed)",
             "step": "pspmm_spmm_run (zero_split + spmm kernels)" if world == 1 else
-                    "all_gather_into_tensor(B) + pspmm_spmm_run on the local shard",
+                    ("all_gather_into_tensor(B) then pspmm_spmm_run on the local shard"
+                     if args.no_overlap else
+                     "async all_gather_into_tensor(B) || own-column block SpMM, then "
+                     "remote-column block pspmm_spmm_accumulate"),
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -465,11 +471,20 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
         run = pdist.ShardedSpmm(sh, K, cfg, stream=stream)
     B = gen.config_B(g.name, g.n)
     B_loc = pdist.pad_rows(torch.from_numpy(B[sh.lo:sh.hi]).cuda(), sh.n_max)
-    A_launch = 1 + (1 if (run.A.info["S"] == 1 and run.A.info["num_chunks"] >
-                          run.A.info["num_panels"]) else 0)
+    def launches(h):  # engine kernel + the split-panel zeroing kernel when present
+        return 1 + (1 if (h.info["S"] == 1 and h.info["num_chunks"] > h.info["num_panels"])
+                    else 0)
+
+    if not args.no_overlap and run.A_own is not None and args.dist_backend == "nccl":
+        A_launch = launches(run.A_own) + (1 if run.A_rem is not None else 0)
+    else:
+        A_launch = launches(run.A)
 
     def step():
-        run.step(B_loc, stream)
+        if args.no_overlap:
+            run.step(B_loc, stream)
+        else:
+            run.step_overlap(B_loc, stream)
 
     def kernel_only():
         run.A.run(run.B_full, run.C, cfg, stream)
@@ -491,7 +506,7 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
 
     def e2e_step():
         dB[: sh.rows].copy_(hB, non_blocking=True)
-        run.step(dB, stream)
+        run.step(dB, stream) if args.no_overlap else run.step_overlap(dB, stream)
         hC.copy_(run.C[: sh.rows], non_blocking=True)
 
     with torch.cuda.stream(stream):

@@ -184,6 +184,17 @@ pspmm_status pspmm_spmm_run(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t
                             int64_t ldc, pspmm_config cfg, void *stream);
 
 /*
+ * C += A . B (beta = 1): same engines and config rules as pspmm_spmm_run,
+ * but every C element is read and accumulated (sole-owner stores read
+ * first; split-panel chunks accumulate with vector atomics as usual and
+ * nothing is zeroed).  Used by the multi-GPU path to add the remote-column
+ * block of a row shard onto its local-column block.
+ * Asynchronous; allocates nothing.
+ */
+pspmm_status pspmm_spmm_accumulate(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
+                                   float *d_C, int64_t ldc, pspmm_config cfg, void *stream);
+
+/*
  * End-to-end variant for host-resident B and C (bench.py "e2e"): copies
  * h_B (n x K, ldb) into the caller's device staging buffer d_Bbuf (same
  * layout), runs the engine into d_Cbuf (ldc) in 8 slices of units cut at

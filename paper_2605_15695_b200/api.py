@@ -104,6 +104,7 @@ _sig("pspmm_pcsr_export", _st, _P, _P, _P, _P, _P)
 _sig("pspmm_pcsr_destroy", None, _P)
 _sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
+_sig("pspmm_spmm_accumulate", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_features_compute", _st, _i64, _i64, _P, _P, _i32, _P, ctypes.POINTER(Features))
 _sig("pspmm_csr_transpose", _st, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P)
 _sig("pspmm_reorder", _st, _i64, _P, _P, _i32, _P)
@@ -251,6 +252,17 @@ def pspmm_spmm_run(A: Pcsr, B, C, cfg: Config, stream=None, K=None):
         raise ValueError("B / C shapes do not match the PCSR handle and K")
     _check(_lib.pspmm_spmm_run(A.handle, b, ldb, K, c, ldc, cfg, _stream(stream)),
            "pspmm_spmm_run")
+
+
+def pspmm_spmm_accumulate(A: Pcsr, B, C, cfg: Config, stream=None, K=None):
+    """C += A . B."""
+    b, ldb = _dense(B, "B")
+    c, ldc = _dense(C, "C")
+    K = B.shape[1] if K is None else K
+    if C.shape[1] < K or B.shape[0] < A.n_cols or C.shape[0] < A.n_rows:
+        raise ValueError("B / C shapes do not match the PCSR handle and K")
+    _check(_lib.pspmm_spmm_accumulate(A.handle, b, ldb, K, c, ldc, cfg, _stream(stream)),
+           "pspmm_spmm_accumulate")
 
 
 def pspmm_spmm_run_host(A: Pcsr, hB, hC, cfg: Config, dB, dC, stream=None):

@@ -147,6 +147,11 @@ pspmm_status pspmm_spmm_run(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t
   return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream));
 }
 
+pspmm_status pspmm_spmm_accumulate(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
+                                   float *d_C, int64_t ldc, pspmm_config cfg, void *stream) {
+  return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream), 1);
+}
+
 pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, int32_t K,
                                  float *h_C, int64_t ldc, pspmm_config cfg, float *d_Bbuf,
                                  float *d_Cbuf, void *stream) {

@@ -130,10 +130,13 @@ pspmm_status prepare_c(const pspmm_pcsr_s *A, int32_t K, float *d_C, int64_t ldc
 // The engine over units [u0, u1).
 pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *d_B,
                           int64_t ldb, int32_t K, float *d_C, int64_t ldc,
-                          const pspmm_config &cfg, cudaStream_t stream, int64_t u0, int64_t u1) {
+                          const pspmm_config &cfg, cudaStream_t stream, int64_t u0, int64_t u1,
+                          int32_t accumulate) {
   if (A->nnz_v == 0 || u1 <= u0) return PSPMM_OK;
-  if (cfg.mode == 2) return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1);
-  if (cfg.mode == 3) return run_spmm_short(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1);
+  if (cfg.mode == 2)
+    return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate);
+  if (cfg.mode == 3)
+    return run_spmm_short(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate);
   SpmmArgs args;
   args.rowptr = A->d_rowptr;
   args.colidx = A->d_colidx;
@@ -148,6 +151,7 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
   args.units = (int32_t)u1;
   args.units_total = (int32_t)A->num_chunks;
   args.K = K;
+  args.accumulate = accumulate;
   const int64_t groups_per_block = plan.threads / plan.G;
   // groups loop over units (grid-stride): cap the grid at PSPMM_WAVES waves of
   // resident blocks so each group pipelines several units
@@ -164,13 +168,16 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
 }  // namespace
 
 pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
-                      int64_t ldc, const pspmm_config &cfg, cudaStream_t stream) {
+                      int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
+                      int32_t accumulate) {
   Plan plan;
   pspmm_status st = make_plan(A, d_B, ldb, K, d_C, ldc, cfg, &plan);
   if (st != PSPMM_OK) return st;
-  st = prepare_c(A, K, d_C, ldc, stream);
-  if (st != PSPMM_OK) return st;
-  return launch_range(A, plan, d_B, ldb, K, d_C, ldc, cfg, stream, 0, A->num_chunks);
+  if (!accumulate) {  // C = A.B: zero what the atomics accumulate into (c-12)
+    st = prepare_c(A, K, d_C, ldc, stream);
+    if (st != PSPMM_OK) return st;
+  }
+  return launch_range(A, plan, d_B, ldb, K, d_C, ldc, cfg, stream, 0, A->num_chunks, accumulate);
 }
 
 pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32_t K, float *h_C,
@@ -192,7 +199,7 @@ pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32
   if (st != PSPMM_OK) return st;
   for (int k = 0; k < kSlices; ++k) {
     st = launch_range(A, plan, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, stream, A->slice_units[k],
-                      A->slice_units[k + 1]);
+                      A->slice_units[k + 1], 0);
     if (st != PSPMM_OK) return st;
     PSPMM_CUDA_TRY(cudaEventRecord(A->slice_done[k], stream));
     PSPMM_CUDA_TRY(cudaStreamWaitEvent(A->copy_stream, A->slice_done[k], 0));

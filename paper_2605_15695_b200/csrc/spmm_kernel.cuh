@@ -41,6 +41,7 @@ struct SpmmArgs {
   float *__restrict__ C;
   int64_t ldb, ldc;
   int32_t n_rows, unit_begin, units, units_total, K;  // units = end of this launch's range
+  int32_t accumulate;                                  // 1: C += A.B
 };
 
 // L2 policies: A (colIdx / val) is streamed once -> evict_first and no L1
@@ -94,8 +95,22 @@ __device__ __forceinline__ float zero_v<float>() {
   return 0.f;
 }
 
-__device__ __forceinline__ void st_c(float4 *p, const float4 &v) { __stcs(p, v); }
-__device__ __forceinline__ void st_c(float *p, const float &v) { __stcs(p, v); }
+// C store; with `accumulate` (pspmm_spmm_accumulate: C += A.B) the old value
+// is added first — one writer per element within a launch, so no atomics
+__device__ __forceinline__ void st_c(float4 *p, float4 v, int accumulate = 0) {
+  if (accumulate) {
+    const float4 o = *p;
+    v.x += o.x;
+    v.y += o.y;
+    v.z += o.z;
+    v.w += o.w;
+  }
+  __stcs(p, v);
+}
+__device__ __forceinline__ void st_c(float *p, float v, int accumulate = 0) {
+  if (accumulate) v += *p;
+  __stcs(p, v);
+}
 __device__ __forceinline__ void red_c(float4 *p, const float4 &v) { atomicAdd(p, v); }
 __device__ __forceinline__ void red_c(float *p, const float &v) { atomicAdd(p, v); }
 
@@ -286,7 +301,7 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
         T *crow = reinterpret_cast<T *>(a.C + row * a.ldc);
 #pragma unroll
         for (int f = 0; f < F; ++f)
-          if (cok[f]) st_c(crow + coff[f] / VW, acc[k][f]);
+          if (cok[f]) st_c(crow + coff[f] / VW, acc[k][f], a.accumulate);
       }
     }
   } else {
@@ -302,7 +317,7 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
         for (int f = 0; f < F; ++f)
           if (cok[f]) {
             if (sole)
-              st_c(crow + coff[f] / VW, acc[k][f]);
+              st_c(crow + coff[f] / VW, acc[k][f], a.accumulate);
             else
               red_c(crow + coff[f] / VW, acc[k][f]);
           }

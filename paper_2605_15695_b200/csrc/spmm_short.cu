@@ -24,6 +24,7 @@ struct ShortArgs {
   float *__restrict__ C;
   int64_t ldb, ldc;
   int32_t row_begin, row_end, K;
+  int32_t accumulate;  // 1: C += A.B
 };
 
 __device__ __forceinline__ int lda(const int32_t *p) {
@@ -125,7 +126,17 @@ __global__ void __launch_bounds__(256, 4) spmm_short_kernel(const ShortArgs a) {
     float4 *crow = reinterpret_cast<float4 *>(a.C + r * a.ldc + col0 + l * 4);
 #pragma unroll
     for (int f = 0; f < F; ++f)
-      if (cok[f]) __stcs(crow + f * G, acc[f]);
+      if (cok[f]) {
+        float4 v = acc[f];
+        if (a.accumulate) {
+          const float4 o = crow[f * G];
+          v.x += o.x;
+          v.y += o.y;
+          v.z += o.z;
+          v.w += o.w;
+        }
+        __stcs(crow + f * G, v);
+      }
     h0 = h1;
     t0 = t1;
     h1 = h2;
@@ -176,7 +187,7 @@ bool short_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc,
 
 pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
                             float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
-                            int64_t u0, int64_t u1) {
+                            int64_t u0, int64_t u1, int32_t accumulate) {
   if (u1 <= u0) return PSPMM_OK;
   const int F = cfg.F;
   int G = cfg.G ? cfg.G : ceil_pow2((K / 4 + F - 1) / F);
@@ -194,6 +205,7 @@ pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb
   args.row_begin = (int32_t)u0;
   args.row_end = (int32_t)u1;
   args.K = K;
+  args.accumulate = accumulate;
   const int threads = std::min(cfg.W, 8) * 32;
   const int64_t per_block = threads / 32 * (32 / G);
   // a few waves of resident blocks (256 x 4 launch bounds: 32 warps / SM)

@@ -118,6 +118,14 @@ class ShardedSpmm:
         self.cfg = cfg
         self.A = api.pspmm_pcsr_build(shard.rows, nnz, rp, ci, vl, cfg.V, cfg.S, cfg.omega,
                                       cfg.sg_override, stream, n_cols=shard.n_cols)
+        # overlap split: the own-column block needs only this rank's B rows,
+        # so it runs while the all-gather of the peers' rows is in flight
+        own, rem = split_own_columns(shard)
+        self.A_own = self.A_rem = None
+        if own[2].shape[0] and shard.world > 1:
+            self.A_own = _build(own, shard.rows, shard.rows, cfg, device, stream)
+            if rem[2].shape[0]:
+                self.A_rem = _build(rem, shard.rows, shard.n_cols, cfg, device, stream)
         self.B_full = torch.empty((shard.n_cols, K), dtype=torch.float32, device=device)
         self.C = torch.empty((shard.n_max, K), dtype=torch.float32, device=device)
         self.C[shard.rows:].zero_()
@@ -128,3 +136,45 @@ class ShardedSpmm:
         all_gather_rows(B_padded, self.B_full, group)
         self.A.run(self.B_full, self.C, self.cfg, stream)
         return self.C
+
+    def step_overlap(self, B_padded, stream=None, group=None):
+        """Same result as step(): C = A_own . B_local while NCCL gathers the
+        peers' rows, then C += A_rem . B_full (pspmm_spmm_accumulate)."""
+        import torch.distributed as dist
+        if self.A_own is None or dist.get_backend(group) != "nccl":
+            return self.step(B_padded, stream, group)
+        work = dist.all_gather_into_tensor(self.B_full, B_padded, group=group, async_op=True)
+        self.A_own.run(B_padded, self.C, self.cfg, stream)
+        work.wait()  # the compute stream waits for the gathered rows
+        if self.A_rem is not None:
+            api.pspmm_spmm_accumulate(self.A_rem, self.B_full, self.C, self.cfg, stream)
+        return self.C
+
+
+def split_own_columns(shard: Shard):
+    """Local CSR split into (own, remote) column blocks, both canonical:
+    own = columns owned by this rank, remapped to local row indices of B
+    (col - rank * n_max); remote = the other columns, in the gathered layout.
+    Each is (rowptr, colidx, val) numpy."""
+    lo = shard.rank * shard.n_max
+    ci = shard.colidx.astype(np.int64)
+    mine = (ci >= lo) & (ci < lo + shard.rows)
+    deg = np.diff(shard.rowptr.astype(np.int64))
+    rows = np.repeat(np.arange(shard.rows), deg)
+
+    def part(mask, shift):
+        counts = np.bincount(rows[mask], minlength=shard.rows)
+        rp = np.zeros(shard.rows + 1, np.int64)
+        np.cumsum(counts, out=rp[1:])
+        return (rp.astype(np.int32), (ci[mask] - shift).astype(np.int32), shard.val[mask])
+
+    return part(mine, lo), part(~mine, 0)
+
+
+def _build(part, n_rows, n_cols, cfg, device, stream):
+    import torch
+    rp, ci, vl = part
+    return api.pspmm_pcsr_build(
+        n_rows, int(rp[-1]), torch.from_numpy(rp).to(device), torch.from_numpy(ci).to(device),
+        torch.from_numpy(vl).to(device), cfg.V, cfg.S, cfg.omega, cfg.sg_override, stream,
+        n_cols=n_cols)

@@ -120,6 +120,27 @@ def test_shard_extract_remap(P):
             assert np.all(np.diff(lci[lrp[i]:lrp[i + 1]]) > 0)
 
 
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_own_remote_column_split(P):
+    """dist.split_own_columns: the two blocks partition every row's nonzeros,
+    the own block is remapped to local B rows, both stay canonical."""
+    import gen
+    from paper_2605_15695_b200 import dist
+    g = gen.community(500, 25, 9, 0.7, 12)
+    for r in range(P):
+        sh = dist.make_shard(g.rowptr, g.colidx, g.val, P, r, align=2)
+        (orp, oci, ovl), (rrp, rci, rvl) = dist.split_own_columns(sh)
+        assert np.array_equal(np.diff(orp) + np.diff(rrp), np.diff(sh.rowptr))
+        lo = r * sh.n_max
+        for i in range(sh.rows):
+            full = sh.colidx[sh.rowptr[i]:sh.rowptr[i + 1]]
+            own = oci[orp[i]:orp[i + 1]]
+            rem = rci[rrp[i]:rrp[i + 1]]
+            assert np.all(np.diff(own) > 0) and np.all(np.diff(rem) > 0)
+            assert np.all((own >= 0) & (own < sh.rows))
+            assert sorted(np.concatenate([own + lo, rem]).tolist()) == full.tolist()
+
+
 def test_product_path_never_touches_oracle():
     """The product (package + native sources) never imports, links or loads
     the oracle, and the oracle never includes the product's headers."""
