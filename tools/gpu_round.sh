@@ -43,6 +43,14 @@ if want corpus; then
   timeout 3000 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --Ws 2,4 --modes 0,2 \
       --out $O/sweep_corpus.json > $O/sweep_corpus.log 2>&1
 fi
+if want sweep3; then
+  # engine mode 3 (V = 1, S = 0 only): merged into the records above by
+  # (graph, K) when the decider is trained
+  timeout 900 python tools/sweep.py --workloads cora,roadnet,reddit,proteins,products --iters 5 \
+      --VS 10 --modes 3 --out $O/sweep_workloads_m3.json > $O/sweep_workloads_m3.log 2>&1
+  timeout 1800 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --VS 10 \
+      --modes 3 --out $O/sweep_corpus_m3.json > $O/sweep_corpus_m3.log 2>&1
+fi
 # never let gpurun_out/ exceed the 64 MiB merge limit
 if [ "$(du -sm $O | cut -f1)" -gt 56 ]; then rm -f $O/*.ncu-rep; fi
 echo done > $O/round_done.txt

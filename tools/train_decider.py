@@ -127,7 +127,7 @@ def fit(X, perf, depth, min_leaf, rng=None, mtry=None):
     return node
 
 
-def fit_forest(X, perf, trees, depth, min_leaf, seed=2605):
+def fit_forest(X, perf, trees, depth, min_leaf, seed=2605, mtry=None):
     """Random forest of cost-sensitive trees: bootstrap records,
     random feature subsets per split; prediction = majority vote."""
     if trees <= 1:
@@ -136,7 +136,7 @@ def fit_forest(X, perf, trees, depth, min_leaf, seed=2605):
     out = []
     for _ in range(trees):
         idx = rng.integers(0, len(X), len(X))
-        out.append(fit(X[idx], perf[idx], depth, min_leaf, rng))
+        out.append(fit(X[idx], perf[idx], depth, min_leaf, rng, mtry))
     return out
 
 
@@ -229,9 +229,10 @@ def emit_header(path, keys, model, source):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("inputs", nargs="+")
-    ap.add_argument("--depth", type=int, default=6)
-    ap.add_argument("--min-leaf", type=int, default=3)
-    ap.add_argument("--trees", type=int, default=32, help="forest size (1 = a single CART tree)")
+    ap.add_argument("--depth", type=int, default=8)
+    ap.add_argument("--min-leaf", type=int, default=2)
+    ap.add_argument("--trees", type=int, default=48, help="forest size (1 = a single CART tree)")
+    ap.add_argument("--mtry", type=int, default=9, help="candidate features per split")
     ap.add_argument("--out-header", default=os.path.join(ROOT, "paper_2605_15695_b200", "csrc",
                                                          "decider_model.h"))
     ap.add_argument("--eval-json", default=None)
@@ -249,7 +250,7 @@ def main():
                           "rnd = a uniformly random valid lattice config; rule = the untrained "
                           "decide.cpp rule"}
     for name, trees in (("tree", 1), ("forest", a.trees)):
-        model = fit_forest(X[tr], perf[tr], trees, a.depth, a.min_leaf)
+        model = fit_forest(X[tr], perf[tr], trees, a.depth, a.min_leaf, mtry=a.mtry)
         per_k = {}
         for K in sorted({r["K"] for r in recs}):
             idx = [i for i in te if recs[i]["K"] == K]
@@ -259,7 +260,7 @@ def main():
                         "train": evaluate(recs, keys, X, perf, tr, model),
                         "held_out_per_K": per_k}
     # the shipped model: the forest, refit on all records
-    model = fit_forest(X, perf, a.trees, a.depth, a.min_leaf)
+    model = fit_forest(X, perf, a.trees, a.depth, a.min_leaf, mtry=a.mtry)
     emit_header(a.out_header, keys, model, ",".join(a.inputs))
     print(json.dumps(report, indent=1))
     if a.eval_json:
