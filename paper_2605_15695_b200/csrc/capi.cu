@@ -133,6 +133,7 @@ void pspmm_pcsr_destroy(pspmm_pcsr A) {
   cudaFree(A->d_val);
   cudaFree(A->d_trow);
   cudaFree(A->d_split);
+  cudaFree(A->d_order);
   if (A->copy_stream) {
     cudaStreamSynchronize(A->copy_stream);
     cudaStreamDestroy(A->copy_stream);

@@ -25,6 +25,7 @@ struct pspmm_pcsr_s {
   float *d_val = nullptr;       // nnz_v * V
   int32_t *d_trow = nullptr;    // num_chunks (S = 1)
   int32_t *d_split = nullptr;   // num_split (S = 1)
+  int32_t *d_order = nullptr;   // num_chunks unit ids by descending vector count (engine schedule)
   int64_t slice_units[kSlices + 1] = {};
   int64_t slice_rows[kSlices + 1] = {};
   cudaStream_t copy_stream = nullptr;  // created lazily by pspmm_spmm_run_host

@@ -206,6 +206,41 @@ pspmm_status exclusive_scan(const int64_t *d_in, int64_t *d_out, int64_t count,
   return PSPMM_OK;
 }
 
+__global__ void unit_len_kernel(int64_t units, const int32_t *__restrict__ rowptr,
+                                int32_t *__restrict__ len, int32_t *__restrict__ ids) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    len[u] = rowptr[u + 1] - rowptr[u];
+    ids[u] = (int32_t)u;
+  }
+}
+
+// Engine schedule (not part of the PCSR contract): unit ids by descending
+// vector count, ties in ascending id (stable radix sort -> deterministic).
+pspmm_status build_unit_order(pspmm_pcsr_s *A, cudaStream_t stream) {
+  const int64_t units = A->num_chunks;
+  if (units < 1) return PSPMM_OK;
+  int32_t *len = nullptr, *len_sorted = nullptr, *ids = nullptr;
+  void *tmp = nullptr;
+  size_t bytes = 0;
+  PSPMM_CUDA_TRY(cudaMalloc(&A->d_order, (size_t)units * sizeof(int32_t)));
+  PSPMM_CUDA_TRY(cudaMallocAsync(&len, (size_t)units * sizeof(int32_t), stream));
+  PSPMM_CUDA_TRY(cudaMallocAsync(&len_sorted, (size_t)units * sizeof(int32_t), stream));
+  PSPMM_CUDA_TRY(cudaMallocAsync(&ids, (size_t)units * sizeof(int32_t), stream));
+  unit_len_kernel<<<grid_for(units, kBlock), kBlock, 0, stream>>>(units, A->d_rowptr, len, ids);
+  PSPMM_CUDA_TRY(cudaGetLastError());
+  PSPMM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, len, len_sorted, ids,
+                                                           A->d_order, (int)units, 0, 32, stream));
+  PSPMM_CUDA_TRY(cudaMallocAsync(&tmp, bytes > 0 ? bytes : 16, stream));
+  PSPMM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, len, len_sorted, ids,
+                                                           A->d_order, (int)units, 0, 32, stream));
+  PSPMM_CUDA_TRY(cudaFreeAsync(tmp, stream));
+  PSPMM_CUDA_TRY(cudaFreeAsync(len, stream));
+  PSPMM_CUDA_TRY(cudaFreeAsync(len_sorted, stream));
+  PSPMM_CUDA_TRY(cudaFreeAsync(ids, stream));
+  return PSPMM_OK;
+}
+
 struct Scratch {
   cudaStream_t s;
   void *ptrs[8] = {};
@@ -310,6 +345,8 @@ pspmm_status build_pcsr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32
     PSPMM_CUDA_TRY(cudaMalloc(&A->d_rowptr, (size_t)(P + 1) * sizeof(int32_t)));
     narrow_kernel<<<grid_for(P + 1, kBlock), kBlock, 0, stream>>>(P + 1, panelptr, A->d_rowptr);
     PSPMM_CUDA_TRY(cudaGetLastError());
+    st = build_unit_order(A, stream);
+    if (st != PSPMM_OK) return st;
     PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
     for (int k = 0; k <= kSlices; ++k) {
       const int64_t p = P * k / kSlices;
@@ -359,6 +396,8 @@ pspmm_status build_pcsr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32
   chunk_fill_kernel<<<grid_for(P, kBlock), kBlock, 0, stream>>>(
       P, SG, nnz_v, panelptr, choff, splitoff, A->d_rowptr, A->d_trow, A->d_split);
   PSPMM_CUDA_TRY(cudaGetLastError());
+  st = build_unit_order(A, stream);
+  if (st != PSPMM_OK) return st;
   // slice bounds at panel boundaries: unit = first chunk of the panel
   for (int k = 0; k <= kSlices; ++k) {
     const int64_t p = P * k / kSlices;

@@ -152,6 +152,9 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
   args.units_total = (int32_t)A->num_chunks;
   args.K = K;
   args.accumulate = accumulate;
+  // the length-sorted unit order applies to whole-matrix launches only (the
+  // host entry's slices are contiguous unit ranges)
+  args.order = (PSPMM_USE_ORDER && u0 == 0 && u1 == A->num_chunks) ? A->d_order : nullptr;
   const int64_t groups_per_block = plan.threads / plan.G;
   // groups loop over units (grid-stride): cap the grid at PSPMM_WAVES waves of
   // resident blocks so each group pipelines several units

@@ -42,6 +42,7 @@ struct SpmmArgs {
   int64_t ldb, ldc;
   int32_t n_rows, unit_begin, units, units_total, K;  // units = end of this launch's range
   int32_t accumulate;                                  // 1: C += A.B
+  const int32_t *__restrict__ order;                   // optional unit order (nullptr = identity)
 };
 
 // L2 policies: A (colIdx / val) is streamed once -> evict_first and no L1
@@ -212,6 +213,10 @@ __device__ __forceinline__ void mac_tile(const char *__restrict__ bptr, uint32_t
 #ifndef PSPMM_MIN_BLOCKS
 #define PSPMM_MIN_BLOCKS 3
 #endif
+// 1: whole-matrix launches visit units by descending vector count (d_order)
+#ifndef PSPMM_USE_ORDER
+#define PSPMM_USE_ORDER 1
+#endif
 // grid = at most PSPMM_WAVES waves of resident blocks (0 = one group per
 // unit, the default: a grid-stride variant with cross-unit prefetch measured
 // 5-14 % slower, profiles/r01/ab_variants.md)
@@ -238,7 +243,11 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
   const int g = lane / G;
   const int l = lane % G;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t unit = a.unit_begin + warp * GPW + g;
+  // with a unit order (descending vector count, built with the PCSR), the
+  // groups of a warp get units of similar length (less intra-warp idling)
+  // and the longest units start first (shorter tail)
+  const int64_t slot = a.unit_begin + warp * GPW + g;
+  const int64_t unit = (a.order && slot < a.units) ? a.order[slot] : slot;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
   const int col0 = blockIdx.y * (G * F * VW);
   const uint64_t pol_a = policy_evict_first();
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
   const uint32_t stride = (uint32_t)(a.ldb * 4);
 
   int head = 0, tail = 0;
-  if (unit < a.units) {
+  if (slot < a.units) {
     head = a.rowptr[unit];
     tail = a.rowptr[unit + 1];
   }
@@ -292,7 +301,7 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
     }
   }
 
-  if (unit >= a.units) return;
+  if (slot >= a.units) return;
   if (S == 0) {
 #pragma unroll
     for (int k = 0; k < V; ++k) {
