@@ -246,9 +246,11 @@ pspmm_status pspmm_csr_permute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                                void *stream);
 
 /*
- * (f1) Row permutation of a dense n x K fp32 matrix on the device:
+ * (f1) Row permutation of a dense fp32 matrix (K columns) on the device,
+ * for i < n (n = entries of d_perm):
  * inverse == 0: out[perm[i]] = in[i]   (B' = P B before the SpMM)
- * inverse != 0: out[i] = in[perm[i]]   (C = P^T C' after it)
+ * inverse != 0: out[i] = in[perm[i]]   (C = P^T C' after it; also the
+ *               row gather that packs halo rows for the multi-GPU path)
  * in and out must not alias.  Asynchronous on `stream`.
  */
 pspmm_status pspmm_permute_rows(int64_t n, int32_t K, const float *d_in, int64_t ldi,

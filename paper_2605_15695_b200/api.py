@@ -343,13 +343,18 @@ def pspmm_csr_permute(rowptr, colidx, val, perm, stream=None):
 
 
 def pspmm_permute_rows(X, perm, inverse=False, out=None, stream=None):
-    """inverse=False: out[perm[i]] = X[i]; inverse=True: out[i] = X[perm[i]]."""
+    """inverse=False: out[perm[i]] = X[i]; inverse=True: out[i] = X[perm[i]]
+    (a row gather; len(perm) may be smaller than X's row count), i < len(perm)."""
     torch = _torch()
     x, ldi = _dense(X, "X")
+    m = perm.shape[0]
     if out is None:
-        out = torch.empty_like(X)
+        out = torch.empty((m if inverse else X.shape[0], X.shape[1]), dtype=X.dtype,
+                          device=X.device)
     o, ldo = _dense(out, "out")
-    st = _lib.pspmm_permute_rows(X.shape[0], X.shape[1], x, ldi, _dev(perm, torch.int32, "perm"),
+    if (not inverse and m > X.shape[0]) or (inverse and m > out.shape[0]):
+        raise ValueError("perm longer than the matrix it indexes")
+    st = _lib.pspmm_permute_rows(m, X.shape[1], x, ldi, _dev(perm, torch.int32, "perm"),
                                  o, ldo, 1 if inverse else 0, _stream(stream))
     _check(st, "pspmm_permute_rows")
     return out

@@ -178,3 +178,159 @@ def _build(part, n_rows, n_cols, cfg, device, stream):
         n_rows, int(rp[-1]), torch.from_numpy(rp).to(device), torch.from_numpy(ci).to(device),
         torch.from_numpy(vl).to(device), cfg.V, cfg.S, cfg.omega, cfg.sg_override, stream,
         n_cols=n_cols)
+
+
+# ---------------------------------------------------------------------------
+# Halo exchange (SURVEY §8(f) f2 ii): each rank receives only the B rows its
+# shard's columns reference, instead of the whole all-gathered B.  For a
+# locality-ordered graph (roadNet: columns within ~sqrt(n) of the row) the
+# halo is a thin band at each shard boundary; for a shuffled power-law graph
+# it approaches all of B and the all-gather (NCCL's fastest collective) wins,
+# so `halo_fraction` lets the caller choose.
+# ---------------------------------------------------------------------------
+@dataclass
+class HaloPlan:
+    rank: int
+    world: int
+    bounds: np.ndarray      # P + 1 row bounds
+    rows: int               # local rows
+    rowptr: np.ndarray      # local CSR with columns in [0, rows + n_halo)
+    colidx: np.ndarray
+    val: np.ndarray
+    recv_counts: list       # rows received from each peer (halo, owner order)
+    send_idx: np.ndarray    # local row ids to send, peers concatenated in rank order
+    send_counts: list
+
+    @property
+    def n_halo(self) -> int:
+        return int(sum(self.recv_counts))
+
+
+def halo_fraction(rowptr, colidx, bounds, rank) -> float:
+    """Halo rows / remote rows for this rank's shard (1.0 = needs all of B)."""
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    cols = np.asarray(colidx[rowptr[lo]:rowptr[hi]], dtype=np.int64)
+    remote = cols[(cols < lo) | (cols >= hi)]
+    n_remote = int(bounds[-1]) - (hi - lo)
+    return len(np.unique(remote)) / max(1, n_remote)
+
+
+def _halo_local(rowptr, colidx, val, bounds, rank):
+    """This rank's side of the plan: local CSR over [own rows | halo] (canonical)
+    and the halo rows it needs, as (owner, owner-local row) ascending."""
+    world = len(bounds) - 1
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    base = int(rowptr[lo])
+    lrp = (np.asarray(rowptr[lo:hi + 1], dtype=np.int64) - base)
+    cols = np.asarray(colidx[base:int(rowptr[hi])], dtype=np.int64)
+    vals = np.asarray(val[base:int(rowptr[hi])], dtype=np.float32)
+    remote = (cols < lo) | (cols >= hi)
+    need = np.unique(cols[remote])                       # ascending = owner order
+    owner = np.searchsorted(bounds, need, side="right") - 1
+    recv_counts = np.bincount(owner, minlength=world).astype(np.int64)
+    # local column ids: own rows first, then the halo in `need` order
+    new_cols = np.where(remote, (hi - lo) + np.searchsorted(need, cols), cols - lo)
+    # keep the local CSR canonical: re-sort every row by its new column ids
+    lrows = np.repeat(np.arange(hi - lo, dtype=np.int64), np.diff(lrp))
+    order = np.argsort(lrows * (hi - lo + len(need) + 1) + new_cols, kind="stable")
+    new_cols, vals = new_cols[order], vals[order]
+    req_local = (need - bounds[owner]).astype(np.int64)
+    return (hi - lo, lrp.astype(np.int32), new_cols.astype(np.int32), vals, recv_counts,
+            req_local)
+
+
+def make_halo_plan(rowptr, colidx, val, world: int, rank: int, group=None,
+                   align: int = 2) -> HaloPlan:
+    """Host preprocessing, once per graph: the rank's rows, the remote rows it
+    needs (grouped by owner, ascending), and — via one all_to_all of counts
+    and one of indices — the rows each peer needs from it."""
+    import torch
+    import torch.distributed as dist
+    bounds = api.pspmm_shard_plan(rowptr, world, align)
+    rows, lrp, cols, vals, recv_counts, req_local = _halo_local(rowptr, colidx, val, bounds, rank)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    cnt_out = torch.from_numpy(recv_counts.copy()).to(dev)
+    cnt_in = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_to_all_single(cnt_in, cnt_out, group=group)
+    send_counts = cnt_in.cpu().numpy().astype(np.int64)
+    idx_in = torch.empty(int(send_counts.sum()), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(idx_in, torch.from_numpy(req_local).to(dev),
+                           output_split_sizes=send_counts.tolist(),
+                           input_split_sizes=recv_counts.tolist(), group=group)
+    return HaloPlan(rank, world, bounds, rows, lrp, cols, vals, recv_counts.tolist(),
+                    idx_in.cpu().numpy().astype(np.int32), send_counts.tolist())
+
+
+def simulate_halo_plans(rowptr, colidx, val, world: int, align: int = 2):
+    """All ranks' HaloPlans computed in one process (the request exchange done
+    by transposing the lists) — single-GPU tests of the halo path."""
+    bounds = api.pspmm_shard_plan(rowptr, world, align)
+    local = [_halo_local(rowptr, colidx, val, bounds, r) for r in range(world)]
+    plans = []
+    for r in range(world):
+        rows, lrp, cols, vals, recv_counts, _ = local[r]
+        send_idx, send_counts = [], []
+        for q in range(world):  # rows rank q asks from rank r, in q's order
+            rq, req = local[q][4], local[q][5]
+            start = int(rq[:r].sum())
+            part = req[start:start + int(rq[r])]
+            send_idx.append(part)
+            send_counts.append(len(part))
+        plans.append(HaloPlan(r, world, bounds, rows, lrp, cols, vals, recv_counts.tolist(),
+                              np.concatenate(send_idx).astype(np.int32), send_counts))
+    return plans
+
+
+class HaloSpmm:
+    """One rank's C_r = A[r-rows, :] . B with a halo exchange per step:
+    pack the rows peers asked for (pspmm_permute_rows as a row gather),
+    all_to_all_single them, SpMM over [local rows | halo rows]."""
+
+    def __init__(self, plan: HaloPlan, K: int, cfg: api.Config | None = None, device="cuda",
+                 stream=None):
+        import torch
+        self.plan = plan
+        self.K = K
+        cfg = cfg or api.Config(W=4, F=1, V=1, S=1)
+        self.cfg = cfg
+        nnz = int(plan.rowptr[-1])
+        self.A = api.pspmm_pcsr_build(
+            plan.rows, nnz, torch.from_numpy(plan.rowptr).to(device),
+            torch.from_numpy(plan.colidx if nnz else np.zeros(1, np.int32)).to(device),
+            torch.from_numpy(plan.val if nnz else np.zeros(1, np.float32)).to(device),
+            cfg.V, cfg.S, cfg.omega, cfg.sg_override, stream, n_cols=plan.rows + plan.n_halo)
+        # B_ext = [local rows | halo]; the next layer writes its C into the first part
+        self.B_ext = torch.zeros((plan.rows + plan.n_halo, K), dtype=torch.float32, device=device)
+        self.send_idx = torch.from_numpy(plan.send_idx.astype(np.int32)).to(device)
+        self.send_buf = torch.empty((max(1, len(plan.send_idx)), K), dtype=torch.float32,
+                                    device=device)
+        self.C = torch.empty((plan.rows, K), dtype=torch.float32, device=device)
+
+    @property
+    def B_local(self):
+        return self.B_ext[: self.plan.rows]
+
+    def exchange(self, group=None, stream=None):
+        import torch
+        import torch.distributed as dist
+        p = self.plan
+        if len(p.send_idx):
+            api.pspmm_permute_rows(self.B_local, self.send_idx, inverse=True,
+                                   out=self.send_buf[: len(p.send_idx)], stream=stream)
+        halo = self.B_ext[p.rows:]
+        if dist.get_backend(group) == "nccl":
+            dist.all_to_all_single(halo, self.send_buf[: len(p.send_idx)],
+                                   output_split_sizes=p.recv_counts,
+                                   input_split_sizes=p.send_counts, group=group)
+        else:  # gloo: host staging
+            out = torch.empty((p.n_halo, self.K), dtype=torch.float32)
+            dist.all_to_all_single(out, self.send_buf[: len(p.send_idx)].cpu(),
+                                   output_split_sizes=p.recv_counts,
+                                   input_split_sizes=p.send_counts, group=group)
+            halo.copy_(out)
+
+    def step(self, stream=None, group=None):
+        """B_local must hold this layer's input rows; returns C (rows x K)."""
+        self.exchange(group, stream)
+        self.A.run(self.B_ext, self.C, self.cfg, stream)
+        return self.C
