@@ -328,6 +328,9 @@ def main():
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: all-gather then SpMM, instead of overlapping the all-gather "
                          "with the own-column block")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo"],
+                    help="N>1: B-row exchange (auto: halo when every rank references < 50 %% "
+                         "of the remote rows)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to rehearse the N>1 flow on one GPU")
     args = ap.parse_args()
@@ -397,13 +400,12 @@ def main():
             "workload": workload_desc(g), "n": g.n, "nnz": g.nnz, "K": K,
             "pcsr_config": cfg_d,
             "parallelism": "single GPU" if world == 1 else
-                           f"{world}-way nnz-balanced row shards + NCCL all-gather of B",
+                           f"{world}-way nnz-balanced row shards + "
+                           f"{'halo all_to_all' if head.get('exchange') == 'halo' else 'all-gather'}"
+                           " of B rows (NCCL)",
             "l2": "flushed between timed steps (256 MiB write, untimed)",
             "step": "pspmm_spmm_run (zero_split + spmm kernels)" if world == 1 else
-                    ("all_gather_into_tensor(B) then pspmm_spmm_run on the local shard"
-                     if args.no_overlap else
-                     "async all_gather_into_tensor(B) || own-column block SpMM, then "
-                     "remote-column block pspmm_spmm_accumulate"),
+                    head.get("step_desc"),
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -456,7 +458,11 @@ def max_over_ranks(vals):
 
 
 def run_sharded(g, args, world, rank, stream, flush, sampler):
-    """N > 1: this rank's row shard; step = all-gather(B) + local SpMM."""
+    """N > 1: this rank's row shard of the fixed graph (strong scaling).  Step =
+    exchange of B rows + local SpMM.  Exchange: NCCL all-gather overlapped with
+    the own-column block (default for dense halos such as the shuffled
+    Reddit-shaped graph), or a halo all_to_all of only the referenced rows
+    (locality-ordered graphs); --exchange auto picks by halo volume."""
     import torch
     import torch.distributed as dist
     from paper_2605_15695_b200 import api, dist as pdist
@@ -466,28 +472,60 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
     feats = api.pspmm_features_compute(g.n, g.nnz, rp, ci, stream=stream)
     cfg = api.pspmm_decide_config(feats, K)
     del rp, ci
-    sh = pdist.make_shard(g.rowptr, g.colidx, g.val, world, rank, align=2)
-    with torch.cuda.stream(stream):
-        run = pdist.ShardedSpmm(sh, K, cfg, stream=stream)
     B = gen.config_B(g.name, g.n)
-    B_loc = pdist.pad_rows(torch.from_numpy(B[sh.lo:sh.hi]).cuda(), sh.n_max)
+    bounds = api.pspmm_shard_plan(g.rowptr, world, 2)
+    (frac,) = max_over_ranks([pdist.halo_fraction(g.rowptr, g.colidx, bounds, rank)])
+    use_halo = args.exchange == "halo" or (args.exchange == "auto" and frac < 0.5)
+
     def launches(h):  # engine kernel + the split-panel zeroing kernel when present
         return 1 + (1 if (h.info["S"] == 1 and h.info["num_chunks"] > h.info["num_panels"])
                     else 0)
 
-    if not args.no_overlap and run.A_own is not None and args.dist_backend == "nccl":
-        A_launch = launches(run.A_own) + (1 if run.A_rem is not None else 0)
+    if use_halo:
+        plan = pdist.make_halo_plan(g.rowptr, g.colidx, g.val, world, rank)
+        with torch.cuda.stream(stream):
+            run = pdist.HaloSpmm(plan, K, cfg, stream=stream)
+        lo, rows = int(plan.bounds[rank]), plan.rows
+        run.B_local.copy_(torch.from_numpy(B[lo:lo + rows]))
+        n_cols, nnz_loc = rows + plan.n_halo, int(plan.rowptr[-1])
+        A_launch = launches(run.A) + (1 if len(plan.send_idx) else 0)  # + the pack kernel
+
+        def step():
+            run.step(stream)
+
+        def kernel_only():
+            run.A.run(run.B_ext, run.C, cfg, stream)
+
+        def e2e_body(hB, hC):
+            run.B_local.copy_(hB, non_blocking=True)
+            run.step(stream)
+            hC.copy_(run.C, non_blocking=True)
+        desc = "halo all_to_all_single of the referenced B rows (row-gather pack) + SpMM"
     else:
-        A_launch = launches(run.A)
+        sh = pdist.make_shard(g.rowptr, g.colidx, g.val, world, rank, align=2)
+        with torch.cuda.stream(stream):
+            run = pdist.ShardedSpmm(sh, K, cfg, stream=stream)
+        lo, rows = sh.lo, sh.rows
+        B_loc = pdist.pad_rows(torch.from_numpy(B[lo:lo + rows]).cuda(), sh.n_max)
+        n_cols, nnz_loc = sh.n_cols, int(sh.rowptr[-1])
+        overlap = not args.no_overlap and run.A_own is not None and args.dist_backend == "nccl"
+        A_launch = (launches(run.A_own) + (1 if run.A_rem is not None else 0)) if overlap \
+            else launches(run.A)
+        dB = torch.zeros((sh.n_max, K), device="cuda")
 
-    def step():
-        if args.no_overlap:
-            run.step(B_loc, stream)
-        else:
-            run.step_overlap(B_loc, stream)
+        def step():
+            run.step_overlap(B_loc, stream) if overlap else run.step(B_loc, stream)
 
-    def kernel_only():
-        run.A.run(run.B_full, run.C, cfg, stream)
+        def kernel_only():
+            run.A.run(run.B_full, run.C, cfg, stream)
+
+        def e2e_body(hB, hC):
+            dB[:rows].copy_(hB, non_blocking=True)
+            run.step_overlap(dB, stream) if overlap else run.step(dB, stream)
+            hC.copy_(run.C[:rows], non_blocking=True)
+        desc = ("async all_gather_into_tensor(B) || own-column block SpMM, then remote-column "
+                "block pspmm_spmm_accumulate" if overlap else
+                "all_gather_into_tensor(B) then pspmm_spmm_run on the local shard")
 
     torch.cuda.synchronize()
     dist.barrier()
@@ -497,25 +535,19 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
     torch.cuda.synchronize()
     dist.barrier()
     ms, kms = max_over_ranks([float(np.mean(ts)), float(np.mean(tk))])
-    nnz_loc = int(sh.rowptr[-1])
-    R = algorithmic_bytes(sh.rows, sh.n_cols, nnz_loc, K)
-    # e2e: pinned host B shard -> device, all-gather, SpMM, D2H of the C shard
-    hB = torch.from_numpy(B[sh.lo:sh.hi].copy()).pin_memory()
-    hC = torch.empty((sh.rows, K)).pin_memory()
-    dB = torch.zeros((sh.n_max, K), device="cuda")
-
-    def e2e_step():
-        dB[: sh.rows].copy_(hB, non_blocking=True)
-        run.step(dB, stream) if args.no_overlap else run.step_overlap(dB, stream)
-        hC.copy_(run.C[: sh.rows], non_blocking=True)
-
+    R = algorithmic_bytes(rows, n_cols, nnz_loc, K)
+    # e2e: pinned host B rows of this rank -> device, exchange, SpMM, D2H of its C rows
+    hB = torch.from_numpy(B[lo:lo + rows].copy()).pin_memory()
+    hC = torch.empty((rows, K)).pin_memory()
     with torch.cuda.stream(stream):
-        te = time_steps(e2e_step, max(3, min(args.steps, 10)), 2, flush, stream)
+        te = time_steps(lambda: e2e_body(hB, hC), max(3, min(args.steps, 10)), 2, flush, stream)
     (me,) = max_over_ranks([float(np.mean(te))])
     e2e = {"value": 2.0 * g.nnz * K / (me * 1e-3) / 1e9, "unit": "GFLOP/s",
            "h2d_bytes_per_step": int(hB.numel() * 4), "d2h_bytes_per_step": int(hC.numel() * 4),
-           "ms_per_step": me, "path": "rank shard: H2D B rows, all-gather, spmm, D2H C rows"}
-    head = {"shard_rows": sh.rows, "shard_nnz": nnz_loc, "kernel_ms_max": kms}
+           "ms_per_step": me, "path": "rank shard: H2D B rows, exchange, spmm, D2H C rows"}
+    head = {"shard_rows": rows, "shard_nnz": nnz_loc, "kernel_ms_max": kms,
+            "exchange": "halo" if use_halo else "allgather", "halo_fraction_max": frac,
+            "step_desc": desc}
     return head, ms, kms, R, cfg.as_dict(), A_launch * args.steps, e2e
 
 

@@ -38,13 +38,15 @@ def test_bench_single_gpu_line():
     assert out["cpu_baseline"]["kind"] == "oracle" and out["cpu_baseline"]["cores"] >= 1
 
 
-def test_bench_two_rank_rehearsal_gloo():
+@pytest.mark.parametrize("exchange,port", [("allgather", 29533), ("halo", 29534)])
+def test_bench_two_rank_rehearsal_gloo(exchange, port):
     out = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-                "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py",
+                "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py",
                 "--workload", "cora", "--steps", "3", "--warmup", "3", "--headline-only",
-                "--dist-backend", "gloo"])
+                "--dist-backend", "gloo", "--exchange", exchange])
     assert out["n_gpus"] == 2 and out["value"] > 0
     assert "row shards" in out["config"]["parallelism"]
+    assert ("halo" in out["config"]["parallelism"]) == (exchange == "halo")
 
 
 def test_bench_reference_arm():
