@@ -71,8 +71,13 @@ typedef enum {
  *     2 = CUDA-core engine, B rows gathered by TMA tile::gather4 into a
  *     shared-memory ring per warp (needs K % 32 == 0, ld % 4 == 0, 16-B
  *     aligned B and C, else PSPMM_ERR_UNSUPPORTED; only W applies);
+ *     3 = short-row pipeline for low-degree graphs (V = 1, S = 0, F in
+ *     {1, 2, 4}, 128-bit layout; W, F, G apply);
  *     1 is reserved for a dense-panel tensor-core path and returns
  *     PSPMM_ERR_UNSUPPORTED.
+ *  order  mode 0 only: 1 = visit units by descending vector count (a
+ *     schedule built with the PCSR; helps skewed, shuffled graphs, hurts
+ *     locality-ordered ones), 0 = in storage order.
  * For pspmm_pcsr_build only V, S, omega and sg_override matter.
  */
 typedef struct {
@@ -81,6 +86,7 @@ typedef struct {
   int32_t sg_override;
   int32_t G;
   int32_t mode;
+  int32_t order;
 } pspmm_config;
 
 typedef struct pspmm_pcsr_s *pspmm_pcsr; /* opaque, immutable after build */

@@ -44,10 +44,10 @@ class PspmmError(RuntimeError):
 class Config(ctypes.Structure):
     """pspmm_config: <W, F, V, S> (P:173) + omega, sg_override, G, mode."""
     _fields_ = [(n, ctypes.c_int32) for n in ("W", "F", "V", "S", "omega", "sg_override", "G",
-                                              "mode")]
+                                              "mode", "order")]
 
-    def __init__(self, W=4, F=1, V=1, S=0, omega=32, sg_override=0, G=0, mode=0):
-        super().__init__(W, F, V, S, omega, sg_override, G, mode)
+    def __init__(self, W=4, F=1, V=1, S=0, omega=32, sg_override=0, G=0, mode=0, order=0):
+        super().__init__(W, F, V, S, omega, sg_override, G, mode, order)
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

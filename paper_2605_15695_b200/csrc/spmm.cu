@@ -74,6 +74,7 @@ pspmm_status make_plan(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int
     PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: G must be 0 or a power of two <= 32");
   if ((uint64_t)ldb * 4 >= (1ull << 32))
     PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: ldb * 4 bytes must be < 2^32");
+  if (cfg.order != 0 && cfg.order != 1) PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: order must be 0 or 1");
   if (cfg.mode == 2) {
     if (!tma_supported(K, ldb, ldc, d_B, d_C))
       PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
@@ -154,7 +155,7 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
   args.accumulate = accumulate;
   // the length-sorted unit order applies to whole-matrix launches only (the
   // host entry's slices are contiguous unit ranges)
-  args.order = (PSPMM_USE_ORDER && u0 == 0 && u1 == A->num_chunks) ? A->d_order : nullptr;
+  args.order = (cfg.order && u0 == 0 && u1 == A->num_chunks) ? A->d_order : nullptr;
   const int64_t groups_per_block = plan.threads / plan.G;
   // groups loop over units (grid-stride): cap the grid at PSPMM_WAVES waves of
   // resident blocks so each group pipelines several units

@@ -213,10 +213,6 @@ __device__ __forceinline__ void mac_tile(const char *__restrict__ bptr, uint32_t
 #ifndef PSPMM_MIN_BLOCKS
 #define PSPMM_MIN_BLOCKS 3
 #endif
-// 1: whole-matrix launches visit units by descending vector count (d_order)
-#ifndef PSPMM_USE_ORDER
-#define PSPMM_USE_ORDER 1
-#endif
 // grid = at most PSPMM_WAVES waves of resident blocks (0 = one group per
 // unit, the default: a grid-stride variant with cross-unit prefetch measured
 // 5-14 % slower, profiles/r01/ab_variants.md)

@@ -70,7 +70,7 @@ def test_c_decider_evaluates_the_header_tree():
                  sr2=rng.uniform(1, 2), rho=d / n, b=rng.uniform(0, n), b_max=n - 1, pr1=0.0,
                  pr2=rng.uniform(0, 0.5))
         K = int(rng.choice([8, 16, 32, 48, 64, 96, 128, 160, 256]))
-        mode, V, S, W, F, P = walk(model, f, K)
+        mode, V, S, W, F, P, order = walk(model, f, K)
         c = api.pspmm_decide_config(f, K)
         if mode == 2 and K % 32 == 0:
             assert (c.mode, c.V, c.S, c.W) == (2, V, S, W)
@@ -81,6 +81,7 @@ def test_c_decider_evaluates_the_header_tree():
             if mode == 0:
                 q = (K + 3) // 4
                 assert c.F == F and c.G == ceil_pow2(-(-q // (F * P)))
+                assert c.order == order
 
 
 def test_trainer_recovers_planted_rule():

@@ -51,6 +51,13 @@ if want sweep3; then
   timeout 1800 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --VS 10 \
       --modes 3 --out $O/sweep_corpus_m3.json > $O/sweep_corpus_m3.log 2>&1
 fi
+if want sweep_order; then
+  # mode-0 points with the length-sorted unit order (order = 1); merged by (graph, K)
+  timeout 1200 python tools/sweep.py --workloads cora,roadnet,reddit,proteins,products --iters 5 \
+      --Ws 2,4,8 --orders 1 --out $O/sweep_workloads_o1.json > $O/sweep_workloads_o1.log 2>&1
+  timeout 2400 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --Ws 2,4 \
+      --orders 1 --out $O/sweep_corpus_o1.json > $O/sweep_corpus_o1.log 2>&1
+fi
 # never let gpurun_out/ exceed the 64 MiB merge limit
 if [ "$(du -sm $O | cut -f1)" -gt 56 ]; then rm -f $O/*.ncu-rep; fi
 echo done > $O/round_done.txt

@@ -70,7 +70,8 @@ def corpus_graphs(count, seed=12345):
     return gs
 
 
-def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2, 1)), modes=(0,)):
+def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2, 1)), modes=(0,),
+                orders=(0,)):
     import torch
     from paper_2605_15695_b200 import api
     rp = torch.from_numpy(g.rowptr).cuda()
@@ -86,18 +87,19 @@ def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2,
         C = torch.empty((g.n, K), device="cuda")
         table = []
         for (V, S), A in handles.items():
-            points = [(0, W, F, G) for (W, F, G) in lattice(K, Ws)] if 0 in modes else []
+            points = [(0, W, F, G, o) for (W, F, G) in lattice(K, Ws) for o in orders] \
+                if 0 in modes else []
             if 2 in modes and K % 32 == 0:  # TMA gather engine: only W matters
-                points += [(2, W, 0, 0) for W in (1, 2, 4, 8)
+                points += [(2, W, 0, 0, 0) for W in (1, 2, 4, 8)
                            if W * 8 * 16 * min(K, 256) <= 227 * 1024]
             if 3 in modes and V == 1 and S == 0 and K % 4 == 0:  # short-row engine
                 for F in (1, 2, 4):
                     G = 1
                     while G < -(-(K // 4) // F) and G < 32:
                         G <<= 1
-                    points += [(3, W, F, max(G, 2)) for W in (2, 4, 8)]
-            for (mode, W, F, G) in points:
-                cfg = api.Config(W=W, F=max(F, 1), V=V, S=S, G=G, mode=mode)
+                    points += [(3, W, F, max(G, 2), 0) for W in (2, 4, 8)]
+            for (mode, W, F, G, order) in points:
+                cfg = api.Config(W=W, F=max(F, 1), V=V, S=S, G=G, mode=mode, order=order)
                 evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                        for _ in range(iters)]
                 A.run(B, C, cfg, stream)
@@ -108,7 +110,7 @@ def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2,
                     e1.record(stream)
                 torch.cuda.synchronize()
                 ts = [a.elapsed_time(b) for a, b in evs]
-                table.append({"V": V, "S": S, "W": W, "F": F, "G": G, "mode": mode,
+                table.append({"V": V, "S": S, "W": W, "F": F, "G": G, "mode": mode, "order": order,
                               "ms": float(np.median(ts))})
         best = min(table, key=lambda r: r["ms"])
         recs.append({"graph": g.name, "n": g.n, "nnz": g.nnz, "K": K, "features": feats,
@@ -133,12 +135,14 @@ def main():
     ap.add_argument("--iters", type=int, default=7)
     ap.add_argument("--Ws", default="2,4,8")
     ap.add_argument("--VS", default="10,11,20,21", help="PCSR corners to sweep, e.g. 11,21")
-    ap.add_argument("--modes", default="0", help="engine modes to sweep: 0 (LDG), 2 (TMA)")
+    ap.add_argument("--modes", default="0", help="engine modes to sweep: 0 (LDG), 2 (TMA), 3")
+    ap.add_argument("--orders", default="0", help="mode-0 unit orders to sweep: 0, 1")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     Ws = tuple(int(x) for x in a.Ws.split(","))
     VS = tuple((int(x[0]), int(x[1])) for x in a.VS.split(","))
     modes = tuple(int(x) for x in a.modes.split(","))
+    orders = tuple(int(x) for x in a.orders.split(","))
     stream = torch.cuda.current_stream()
     flush_buf = torch.empty(bench.L2_FLUSH_BYTES // 4, device="cuda")
 
@@ -150,14 +154,14 @@ def main():
     for name in [w for w in a.workloads.split(",") if w]:
         g = bench.load_graph(name)
         Ks = [int(k) for k in a.Ks.split(",")] if a.Ks else [g.K]
-        recs += sweep_graph(g, Ks, a.iters, flush, stream, Ws, VS, modes)
+        recs += sweep_graph(g, Ks, a.iters, flush, stream, Ws, VS, modes, orders)
         print(f"[{time.time() - t0:.0f}s] {name}: best {recs[-1]['best']} "
               f"{recs[-1]['best_gflops']:.0f} GFLOP/s", flush=True)
         json.dump(recs, open(a.out, "w"))
     if a.corpus:
         Ks = [int(k) for k in a.Ks.split(",")] if a.Ks else [16, 32, 64, 128, 256]
         for g in corpus_graphs(a.corpus, a.corpus_seed):
-            recs += sweep_graph(g, Ks, a.iters, flush, stream, Ws, VS, modes)
+            recs += sweep_graph(g, Ks, a.iters, flush, stream, Ws, VS, modes, orders)
             print(f"[{time.time() - t0:.0f}s] {g.name} n={g.n} nnz={g.nnz}", flush=True)
             json.dump(recs, open(a.out, "w"))
     json.dump(recs, open(a.out, "w"))

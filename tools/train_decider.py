@@ -59,11 +59,11 @@ def label_of(K, t):
     not re-derive its G from (K, F, P)."""
     mode = t.get("mode", 0)
     if mode == 2:
-        return (2, t["V"], t["S"], t["W"], 1, 1)
+        return (2, t["V"], t["S"], t["W"], 1, 1, 0)
     P = passes_of(K, t["F"], t["G"])
     if derived_G(K, t["F"], P) != t["G"]:
         return None
-    return (mode, t["V"], t["S"], t["W"], t["F"], P)
+    return (mode, t["V"], t["S"], t["W"], t["F"], P, t.get("order", 0) if mode == 0 else 0)
 
 
 def build_matrix(recs):
@@ -171,7 +171,7 @@ def rule_label(r, keys):
     V = 2 if f["pr2"] < 0.30 else 1
     S = 1 if f["d_max"] > 8.0 * f["d_hat"] else 0
     d = r["decided"]
-    return (0, V, S, 4, d["F"], passes_of(r["K"], d["F"], d["G"]))
+    return (0, V, S, 4, d["F"], passes_of(r["K"], d["F"], d["G"]), 0)
 
 
 def evaluate(recs, keys, X, perf, test_idx, root, seed=0):
@@ -219,8 +219,8 @@ def emit_header(path, keys, model, source):
     lines.append("// leaf -> label id (-1 for inner nodes)")
     lines.append("constexpr int kLeafLabel[kNodes] = {" +
                  ", ".join(str(lid[n.label]) if n.feat < 0 else "-1" for n in nodes) + "};")
-    lines.append("// label: {mode, V, S, W, F, P (column passes)}")
-    lines.append("constexpr int kLabel[kNumLabels][6] = {" +
+    lines.append("// label: {mode, V, S, W, F, P (column passes), order}")
+    lines.append("constexpr int kLabel[kNumLabels][7] = {" +
                  ", ".join("{" + ", ".join(map(str, keys[k])) + "}" for k in used) + "};")
     lines.append("}  // namespace pspmm_model")
     open(path, "w").write("\n".join(lines) + "\n")
