@@ -328,9 +328,12 @@ def main():
     ap.add_argument("--no-overlap", action="store_true",
                     help="N>1: all-gather then SpMM, instead of overlapping the all-gather "
                          "with the own-column block")
-    ap.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo"],
-                    help="N>1: B-row exchange (auto: halo when every rank references < 50 %% "
-                         "of the remote rows)")
+    ap.add_argument("--exchange", default="auto",
+                    choices=["auto", "allgather", "halo", "fanout"],
+                    help="N>1: row exchange (auto: halo when every rank references < 50 %% "
+                         "of the remote rows, else the all-gather fused into the SpMM "
+                         "epilogue (fanout) when the peers map over CUDA IPC, else the "
+                         "overlapped NCCL all-gather)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to rehearse the N>1 flow on one GPU")
     args = ap.parse_args()
@@ -401,8 +404,7 @@ def main():
             "pcsr_config": cfg_d,
             "parallelism": "single GPU" if world == 1 else
                            f"{world}-way nnz-balanced row shards + "
-                           f"{'halo all_to_all' if head.get('exchange') == 'halo' else 'all-gather'}"
-                           " of B rows (NCCL)",
+                           f"{EXCHANGE_DESC[head.get('exchange', 'allgather')]}",
             "l2": "flushed between timed steps (256 MiB write, untimed)",
             "step": "pspmm_spmm_run (zero_split + spmm kernels)" if world == 1 else
                     head.get("step_desc"),
@@ -462,7 +464,12 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
     exchange of B rows + local SpMM.  Exchange: NCCL all-gather overlapped with
     the own-column block (default for dense halos such as the shuffled
     Reddit-shaped graph), or a halo all_to_all of only the referenced rows
-    (locality-ordered graphs); --exchange auto picks by halo volume."""
+    (locality-ordered graphs), or (f2 i) no collective at all: the SpMM epilogue
+    stores every output row into every rank's next-layer B over CUDA-IPC peer
+    memory (FanoutSpmm), followed by a one-element all-reduce barrier.
+    --exchange auto: halo by halo volume, else fanout when the peers map and
+    one validated step matches the plain engine, else the overlapped
+    all-gather."""
     import torch
     import torch.distributed as dist
     from paper_2605_15695_b200 import api, dist as pdist
@@ -476,12 +483,40 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
     bounds = api.pspmm_shard_plan(g.rowptr, world, 2)
     (frac,) = max_over_ranks([pdist.halo_fraction(g.rowptr, g.colidx, bounds, rank)])
     use_halo = args.exchange == "halo" or (args.exchange == "auto" and frac < 0.5)
+    fanout, fanout_note = None, None
+    if not use_halo and args.exchange in ("auto", "fanout") and args.dist_backend == "nccl":
+        fanout, fanout_note = setup_fanout(g, cfg, gen.config_B(g.name, g.n), world, rank,
+                                           stream)
 
     def launches(h):  # engine kernel + the split-panel zeroing kernel when present
         return 1 + (1 if (h.info["S"] == 1 and h.info["num_chunks"] > h.info["num_panels"])
                     else 0)
 
-    if use_halo:
+    if fanout is not None:
+        run = fanout
+        sh = run.shard
+        lo, rows = sh.lo, sh.rows
+        n_cols, nnz_loc = sh.n_cols, int(sh.rowptr[-1])
+        split = run.A.info["S"] == 1 and run.A.info["num_chunks"] > run.A.info["num_panels"]
+        A_launch = 1 + (world if split else 0)  # engine + split-row zeroing per copy
+        C_k = torch.empty((rows, K), device="cuda")
+        dB = torch.zeros((sh.n_max, K), device="cuda")
+
+        def step():  # one layer: SpMM whose epilogue stores every row at every rank
+            run.step(stream, swap=False)
+
+        def kernel_only():
+            run.A.run(run.X[0], C_k, cfg, stream)
+
+        def e2e_body(hB, hC):
+            dB[:rows].copy_(hB, non_blocking=True)
+            pdist.all_gather_rows(dB, run.X[0])
+            run.step(stream, swap=False)
+            hC.copy_(run.own(1), non_blocking=True)
+        desc = ("pspmm_spmm_run_fanout: SpMM whose epilogue stores each output row into "
+                "every rank's next-layer B (CUDA-IPC peer memory over NVLink), then a "
+                "one-element NCCL all-reduce as the layer barrier; no separate collective")
+    elif use_halo:
         plan = pdist.make_halo_plan(g.rowptr, g.colidx, g.val, world, rank)
         with torch.cuda.stream(stream):
             run = pdist.HaloSpmm(plan, K, cfg, stream=stream)
@@ -546,9 +581,67 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
            "h2d_bytes_per_step": int(hB.numel() * 4), "d2h_bytes_per_step": int(hC.numel() * 4),
            "ms_per_step": me, "path": "rank shard: H2D B rows, exchange, spmm, D2H C rows"}
     head = {"shard_rows": rows, "shard_nnz": nnz_loc, "kernel_ms_max": kms,
-            "exchange": "halo" if use_halo else "allgather", "halo_fraction_max": frac,
-            "step_desc": desc}
+            "exchange": "fanout" if fanout is not None else "halo" if use_halo else "allgather",
+            "halo_fraction_max": frac, "step_desc": desc}
+    if fanout_note:
+        head["fanout_note"] = fanout_note
     return head, ms, kms, R, cfg.as_dict(), A_launch * args.steps, e2e
+
+
+EXCHANGE_DESC = {
+    "halo": "halo all_to_all of the referenced B rows (NCCL)",
+    "allgather": "all-gather of B rows (NCCL)",
+    "fanout": "all-gather fused into the SpMM epilogue (P2P stores to every rank's next-layer "
+              "B over CUDA IPC / NVLink)",
+}
+
+
+def setup_fanout(g, cfg, B, world, rank, stream):
+    """Map every peer's gathered buffers (CUDA IPC) and validate one fused
+    step against the plain engine on the same gathered input on all ranks.
+    Returns (FanoutSpmm or None, note); every rank reaches the same decision
+    (failures are max-reduced), so no rank is left waiting in a collective."""
+    import torch
+    from paper_2605_15695_b200 import api, dist as pdist
+    sh = pdist.make_shard(g.rowptr, g.colidx, g.val, world, rank, align=2)
+    with torch.cuda.stream(stream):
+        run = pdist.FanoutSpmm(sh, g.K, cfg, stream=stream)
+    torch.cuda.synchronize()
+    err = ""
+    try:
+        run.connect()
+    except Exception as e:  # e.g. no P2P path between the GPUs
+        err = f"connect: {e!r}"[:200]
+    (bad,) = max_over_ranks([1.0 if err else 0.0])
+    if bad:
+        run.close()
+        return None, err or "a peer rank failed to map the buffers"
+    try:
+        B_loc = pdist.pad_rows(torch.from_numpy(B[sh.lo:sh.hi].copy()).cuda(), sh.n_max)
+        pdist.all_gather_rows(B_loc, run.X[0])
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            run.X[1].zero_()
+            torch.cuda.synchronize()
+            import torch.distributed as tdist
+            tdist.barrier()
+            run.step(stream, swap=False)
+            mine = torch.empty((sh.rows, g.K), device="cuda")
+            api.pspmm_spmm_run(run.A, run.X[0], mine, cfg, stream)
+        torch.cuda.synchronize()
+        # every slot of X[1] must hold its owner's rows: compare with the
+        # all-gather of the plain engine's outputs
+        ref = pdist.all_gather_rows(pdist.pad_rows(mine, sh.n_max))
+        torch.cuda.synchronize()
+        if not torch.allclose(run.X[1], ref, rtol=1e-4, atol=1e-4):
+            err = "validation: fused copies differ from the all-gathered outputs"
+    except Exception as e:
+        err = f"validation: {e!r}"[:200]
+    (bad,) = max_over_ranks([1.0 if err else 0.0])
+    if bad:
+        run.close()
+        return None, err or "validation failed on a peer rank"
+    return run, None
 
 
 def run_reference(args, world, rank):

@@ -215,6 +215,39 @@ pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, in
                                  float *d_Cbuf, void *stream);
 
 /*
+ * (f2 (i): the all-gather fused into the SpMM epilogue)
+ * C = A . B exactly as pspmm_spmm_run, and every C element the engine writes
+ * (stores, split-panel atomics, the zeroing of split rows) is also written at
+ * the same offset relative to each of d_peers[0 .. npeers) — device pointers
+ * this device can store to (peer memory mapped with pspmm_ipc_open over
+ * NVLink, or any other device buffer), each addressed with ldc like d_C.  In
+ * the sharded layer chain d_C is this rank's slot of its own
+ * next-layer B_full and d_peers are the same slot in every peer's B_full, so
+ * the transfer is spread over the kernel's lifetime instead of following it.
+ * Each CTA ends with a system-scope fence; the caller orders the peers'
+ * subsequent reads with a barrier (stream-ordered, e.g. a one-element NCCL
+ * all-reduce).  h_peers is a HOST array of npeers device pointers,
+ * 0 <= npeers <= PSPMM_MAX_PEERS (else PSPMM_ERR_INVALID_ARG).  Asynchronous.
+ */
+#define PSPMM_MAX_PEERS 7
+pspmm_status pspmm_spmm_run_fanout(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
+                                   float *d_C, int64_t ldc, float *const *h_peers, int32_t npeers,
+                                   pspmm_config cfg, void *stream);
+
+/*
+ * CUDA IPC plumbing for the fan-out (f2): export a device allocation made
+ * with cudaMalloc (or any sub-range of one, as caching allocators hand out) as a 64-byte
+ * handle, open a peer process's handle (peer access enabled lazily) and
+ * close it.  pspmm_ipc_get_handle writes 64 bytes to h_handle and the byte
+ * offset of d_ptr inside its allocation to *offset (the handle names the
+ * whole allocation); the opener adds that offset.  A handle cannot be opened
+ * in the process that exported it (CUDA IPC rule) -> PSPMM_ERR_CUDA.
+ */
+pspmm_status pspmm_ipc_get_handle(const void *d_ptr, void *h_handle, int64_t *offset);
+pspmm_status pspmm_ipc_open(const void *h_handle, void **d_base);
+pspmm_status pspmm_ipc_close(void *d_base);
+
+/*
  * (f3) CSR of A^T on the device, for the backward SpMM of a GNN layer
  * (dL/dB = A^T . dL/dC).  A is n_rows x n_cols
  * canonical CSR; the outputs are caller-allocated device arrays:
@@ -275,8 +308,9 @@ pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_row
 
 /*
  * (a3) SpMM-decider stand-in: a pure host function of
- * (features, K) returning a valid <W, F, V, S> (+ G) for K.  The model is a
- * decision tree trained on this repo's own autotune sweep.
+ * (features, K) returning a valid <W, F, V, S> (+ G, engine mode, unit
+ * order) for K.  The model is a random forest trained on this repo's own
+ * B200 autotune sweep, compiled in.
  */
 pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K, pspmm_config *out);
 

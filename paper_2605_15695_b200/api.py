@@ -105,6 +105,10 @@ _sig("pspmm_pcsr_destroy", None, _P)
 _sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
 _sig("pspmm_spmm_accumulate", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
+_sig("pspmm_spmm_run_fanout", _st, _P, _P, _i64, _i32, _P, _i64, _P, _i32, Config, _P)
+_sig("pspmm_ipc_get_handle", _st, _P, _P, ctypes.POINTER(_i64))
+_sig("pspmm_ipc_open", _st, _P, ctypes.POINTER(_P))
+_sig("pspmm_ipc_close", _st, _P)
 _sig("pspmm_features_compute", _st, _i64, _i64, _P, _P, _i32, _P, ctypes.POINTER(Features))
 _sig("pspmm_csr_transpose", _st, _i64, _i64, _i64, _P, _P, _P, _P, _P, _P, _P)
 _sig("pspmm_reorder", _st, _i64, _P, _P, _i32, _P)
@@ -263,6 +267,59 @@ def pspmm_spmm_accumulate(A: Pcsr, B, C, cfg: Config, stream=None, K=None):
         raise ValueError("B / C shapes do not match the PCSR handle and K")
     _check(_lib.pspmm_spmm_accumulate(A.handle, b, ldb, K, c, ldc, cfg, _stream(stream)),
            "pspmm_spmm_accumulate")
+
+
+MAX_PEERS = 7  # PSPMM_MAX_PEERS
+
+
+def pspmm_spmm_run_fanout(A: Pcsr, B, C, peers, cfg: Config, stream=None, K=None):
+    """C = A . B with every written C element also stored at the same offset
+    of each peer buffer (f2).  peers: device addresses (int, e.g. from
+    pspmm_ipc_open plus an offset) or CUDA tensors laid out like C."""
+    b, ldb = _dense(B, "B")
+    c, ldc = _dense(C, "C")
+    K = B.shape[1] if K is None else K
+    if C.shape[1] < K or B.shape[0] < A.n_cols or C.shape[0] < A.n_rows:
+        raise ValueError("B / C shapes do not match the PCSR handle and K")
+    torch = _torch()
+    addrs = []
+    for p in peers:
+        if isinstance(p, torch.Tensor):
+            q, ld = _dense(p, "peer")
+            if ld != ldc or p.shape[0] < A.n_rows:
+                raise ValueError("a peer tensor must be laid out like C")
+            addrs.append(q.value)
+        else:
+            addrs.append(int(p))
+    if len(addrs) > MAX_PEERS:
+        raise ValueError(f"at most {MAX_PEERS} peers")
+    arr = (ctypes.c_void_p * max(1, len(addrs)))(*addrs)
+    _check(_lib.pspmm_spmm_run_fanout(A.handle, b, ldb, K, c, ldc, arr, len(addrs), cfg,
+                                      _stream(stream)), "pspmm_spmm_run_fanout")
+
+
+def pspmm_ipc_get_handle(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding tensor t, byte
+    offset of t inside it)."""
+    buf = ctypes.create_string_buffer(64)
+    off = _i64()
+    _check(_lib.pspmm_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), buf, ctypes.byref(off)),
+           "pspmm_ipc_get_handle")
+    return buf.raw, off.value
+
+
+def pspmm_ipc_open(handle: bytes) -> int:
+    """Map a peer process's allocation; returns its base device address."""
+    if len(handle) != 64:
+        raise ValueError("an IPC handle is 64 bytes")
+    p = _P()
+    _check(_lib.pspmm_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(p)),
+           "pspmm_ipc_open")
+    return p.value
+
+
+def pspmm_ipc_close(base: int):
+    _check(_lib.pspmm_ipc_close(ctypes.c_void_p(base)), "pspmm_ipc_close")
 
 
 def pspmm_spmm_run_host(A: Pcsr, hB, hC, cfg: Config, dB, dC, stream=None):

@@ -1,5 +1,9 @@
 // extern "C" entry points of libpspmm.so (declared in include/pspmm.h).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -15,6 +19,22 @@ pspmm_status cuda_status(cudaError_t e, const char *where) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
   cudaGetLastError();  // clear sticky-free errors
   return e == cudaErrorMemoryAllocation ? PSPMM_ERR_OOM : PSPMM_ERR_CUDA;
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (the library
+// does not link libcuda directly)
+static PFN_cuMemGetAddressRange_v3020 get_address_range() {
+  static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  });
+  return fn;
 }
 
 }  // namespace pspmm
@@ -151,6 +171,60 @@ pspmm_status pspmm_spmm_run(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t
 pspmm_status pspmm_spmm_accumulate(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
                                    float *d_C, int64_t ldc, pspmm_config cfg, void *stream) {
   return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream), 1);
+}
+
+pspmm_status pspmm_spmm_run_fanout(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
+                                   float *d_C, int64_t ldc, float *const *h_peers, int32_t npeers,
+                                   pspmm_config cfg, void *stream) {
+  if (npeers < 0 || npeers > PSPMM_MAX_PEERS || (npeers > 0 && !h_peers)) {
+    set_error("spmm_run_fanout: npeers must be in 0..PSPMM_MAX_PEERS with a peer array");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  Fanout fan{};
+  fan.n = npeers;
+  for (int d = 0; d < npeers; ++d) fan.peer[d] = h_peers[d];
+  return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream), 0, &fan);
+}
+
+pspmm_status pspmm_ipc_get_handle(const void *d_ptr, void *h_handle, int64_t *offset) {
+  if (!d_ptr || !h_handle || !offset) {
+    set_error("ipc_get_handle: null argument");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  auto range = get_address_range();
+  if (!range) {
+    set_error("ipc_get_handle: cuMemGetAddressRange unavailable");
+    return PSPMM_ERR_CUDA;
+  }
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) {
+    set_error("ipc_get_handle: not a device allocation");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  cudaIpcMemHandle_t h;
+  PSPMM_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+  memcpy(h_handle, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+  return PSPMM_OK;
+}
+
+pspmm_status pspmm_ipc_open(const void *h_handle, void **d_base) {
+  if (!h_handle || !d_base) {
+    set_error("ipc_open: null argument");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h_handle, sizeof(h));
+  PSPMM_CUDA_TRY(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
+  return PSPMM_OK;
+}
+
+pspmm_status pspmm_ipc_close(void *d_base) {
+  if (!d_base) return PSPMM_OK;
+  PSPMM_CUDA_TRY(cudaIpcCloseMemHandle(d_base));
+  return PSPMM_OK;
 }
 
 pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, int32_t K,

@@ -75,22 +75,32 @@ pspmm_status build_pcsr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32
 pspmm_status panel_counts_v2(int64_t n_rows, const int32_t *d_rowptr, const int32_t *d_colidx,
                              int32_t *d_L, cudaStream_t stream);
 
+// Output fan-out (f2, pspmm_spmm_run_fanout): every C element the engine
+// writes is also written, at the same offset, to each peer buffer (device
+// pointers this device can store to, e.g. CUDA-IPC-mapped peer memory), and
+// each CTA ends with a system-scope fence.  Passed by value in kernel args.
+constexpr int kMaxPeers = PSPMM_MAX_PEERS;
+struct Fanout {
+  float *peer[kMaxPeers];
+  int32_t n;
+};
+
 // spmm.cu
 pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
                       int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
-                      int32_t accumulate = 0);
+                      int32_t accumulate = 0, const Fanout *fan = nullptr);
 
 // spmm_tma.cu (engine mode 2)
 bool tma_supported(int32_t K, int64_t ldb, int64_t ldc, const float *d_B, const float *d_C);
 pspmm_status run_spmm_tma(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
                           float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
-                          int64_t u0, int64_t u1, int32_t accumulate);
+                          int64_t u0, int64_t u1, int32_t accumulate, const Fanout &fan);
 // spmm_short.cu (engine mode 3)
 bool short_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc, const float *d_B,
                      const float *d_C, const pspmm_config &cfg);
 pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
                             float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
-                            int64_t u0, int64_t u1, int32_t accumulate);
+                            int64_t u0, int64_t u1, int32_t accumulate, const Fanout &fan);
 // host entry: H2D(B), engine in kSlices unit slices, D2H of each slice's C
 // rows on a second stream as soon as the slice is done
 pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32_t K, float *h_C,

@@ -111,19 +111,23 @@ pspmm_status make_plan(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int
 }
 
 // C rows of split panels = 0 (S = 1, c-12); everything else is overwritten.
+// With a fan-out the peer copies are zeroed the same way.
 pspmm_status prepare_c(const pspmm_pcsr_s *A, int32_t K, float *d_C, int64_t ldc,
-                       cudaStream_t stream) {
-  if (A->nnz_v == 0) {
-    const int64_t total = A->n_rows * K;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
-    zero_all_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(A->n_rows, K, d_C, ldc);
-    PSPMM_CUDA_TRY(cudaGetLastError());
-  } else if (A->S == 1 && A->num_split > 0) {
-    const int64_t total = A->num_split * A->V * (int64_t)K;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
-    zero_split_kernel<<<blocks, 256, 0, stream>>>(A->d_split, A->num_split, A->V, A->n_rows, K,
-                                                   d_C, ldc);
-    PSPMM_CUDA_TRY(cudaGetLastError());
+                       cudaStream_t stream, const Fanout &fan) {
+  for (int d = -1; d < fan.n; ++d) {
+    float *C = d < 0 ? d_C : fan.peer[d];
+    if (A->nnz_v == 0) {
+      const int64_t total = A->n_rows * K;
+      const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+      zero_all_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(A->n_rows, K, C, ldc);
+      PSPMM_CUDA_TRY(cudaGetLastError());
+    } else if (A->S == 1 && A->num_split > 0) {
+      const int64_t total = A->num_split * A->V * (int64_t)K;
+      const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+      zero_split_kernel<<<blocks, 256, 0, stream>>>(A->d_split, A->num_split, A->V, A->n_rows,
+                                                     K, C, ldc);
+      PSPMM_CUDA_TRY(cudaGetLastError());
+    }
   }
   return PSPMM_OK;
 }
@@ -132,12 +136,12 @@ pspmm_status prepare_c(const pspmm_pcsr_s *A, int32_t K, float *d_C, int64_t ldc
 pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *d_B,
                           int64_t ldb, int32_t K, float *d_C, int64_t ldc,
                           const pspmm_config &cfg, cudaStream_t stream, int64_t u0, int64_t u1,
-                          int32_t accumulate) {
+                          int32_t accumulate, const Fanout &fan) {
   if (A->nnz_v == 0 || u1 <= u0) return PSPMM_OK;
   if (cfg.mode == 2)
-    return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate);
+    return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate, fan);
   if (cfg.mode == 3)
-    return run_spmm_short(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate);
+    return run_spmm_short(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate, fan);
   SpmmArgs args;
   args.rowptr = A->d_rowptr;
   args.colidx = A->d_colidx;
@@ -153,6 +157,7 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
   args.units_total = (int32_t)A->num_chunks;
   args.K = K;
   args.accumulate = accumulate;
+  args.fan = fan;
   // the length-sorted unit order applies to whole-matrix launches only (the
   // host entry's slices are contiguous unit ranges)
   args.order = (cfg.order && u0 == 0 && u1 == A->num_chunks) ? A->d_order : nullptr;
@@ -173,15 +178,31 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
 
 pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
                       int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
-                      int32_t accumulate) {
+                      int32_t accumulate, const Fanout *fan) {
+  Fanout f{};
+  if (fan) {
+    if (fan->n < 0 || fan->n > kMaxPeers)
+      PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_fanout: npeers must be in 0..PSPMM_MAX_PEERS");
+    if (fan->n > 0 && accumulate)
+      PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run_fanout: no accumulate with peer copies");
+    for (int d = 0; d < fan->n; ++d) {
+      if (!fan->peer[d]) PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_fanout: null peer pointer");
+      // peer copies take the same vector width as C
+      if ((reinterpret_cast<uintptr_t>(fan->peer[d]) & 15) !=
+          (reinterpret_cast<uintptr_t>(d_C) & 15))
+        PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_fanout: peer alignment differs from C's");
+    }
+    f = *fan;
+  }
   Plan plan;
   pspmm_status st = make_plan(A, d_B, ldb, K, d_C, ldc, cfg, &plan);
   if (st != PSPMM_OK) return st;
   if (!accumulate) {  // C = A.B: zero what the atomics accumulate into (c-12)
-    st = prepare_c(A, K, d_C, ldc, stream);
+    st = prepare_c(A, K, d_C, ldc, stream, f);
     if (st != PSPMM_OK) return st;
   }
-  return launch_range(A, plan, d_B, ldb, K, d_C, ldc, cfg, stream, 0, A->num_chunks, accumulate);
+  return launch_range(A, plan, d_B, ldb, K, d_C, ldc, cfg, stream, 0, A->num_chunks, accumulate,
+                      f);
 }
 
 pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32_t K, float *h_C,
@@ -199,11 +220,12 @@ pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32
   }
   PSPMM_CUDA_TRY(cudaMemcpyAsync(d_Bbuf, h_B, (size_t)A->n_cols * ldb * sizeof(float),
                                  cudaMemcpyHostToDevice, stream));
-  st = prepare_c(A, K, d_Cbuf, ldc, stream);
+  const Fanout none{};
+  st = prepare_c(A, K, d_Cbuf, ldc, stream, none);
   if (st != PSPMM_OK) return st;
   for (int k = 0; k < kSlices; ++k) {
     st = launch_range(A, plan, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, stream, A->slice_units[k],
-                      A->slice_units[k + 1], 0);
+                      A->slice_units[k + 1], 0, none);
     if (st != PSPMM_OK) return st;
     PSPMM_CUDA_TRY(cudaEventRecord(A->slice_done[k], stream));
     PSPMM_CUDA_TRY(cudaStreamWaitEvent(A->copy_stream, A->slice_done[k], 0));

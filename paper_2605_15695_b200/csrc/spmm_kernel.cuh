@@ -43,6 +43,7 @@ struct SpmmArgs {
   int32_t n_rows, unit_begin, units, units_total, K;  // units = end of this launch's range
   int32_t accumulate;                                  // 1: C += A.B
   const int32_t *__restrict__ order;                   // optional unit order (nullptr = identity)
+  Fanout fan;                                          // peer copies of C (f2); fan.n = 0: none
 };
 
 // L2 policies: A (colIdx / val) is streamed once -> evict_first and no L1
@@ -114,6 +115,26 @@ __device__ __forceinline__ void st_c(float *p, float v, int accumulate = 0) {
 }
 __device__ __forceinline__ void red_c(float4 *p, const float4 &v) { atomicAdd(p, v); }
 __device__ __forceinline__ void red_c(float *p, const float &v) { atomicAdd(p, v); }
+
+// Write one C element group at float offset `off`: to C (store or atomic) and,
+// with a fan-out, to the same offset of every peer buffer (f2).  The peer
+// loop is a uniform branch on a kernel parameter: free when fan.n == 0.
+template <typename T>
+__device__ __forceinline__ void put_c(const SpmmArgs &a, int64_t off, const T &v, bool red) {
+  T *p = reinterpret_cast<T *>(a.C + off);
+  if (red)
+    red_c(p, v);
+  else
+    st_c(p, v, a.accumulate);
+#pragma unroll 1
+  for (int d = 0; d < a.fan.n; ++d) {
+    T *q = reinterpret_cast<T *>(a.fan.peer[d] + off);
+    if (red)
+      red_c(q, v);
+    else
+      st_c(q, v, 0);
+  }
+}
 
 // Stage one tile of the unit's vectors: lane l of the group holds vectors
 // base + m G + l, m < M (colIdx and the V values; Alg. 2 l.6-7).
@@ -303,10 +324,9 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
     for (int k = 0; k < V; ++k) {
       const int64_t row = unit * V + k;
       if (row < a.n_rows) {
-        T *crow = reinterpret_cast<T *>(a.C + row * a.ldc);
 #pragma unroll
         for (int f = 0; f < F; ++f)
-          if (cok[f]) st_c(crow + coff[f] / VW, acc[k][f], a.accumulate);
+          if (cok[f]) put_c(a, row * a.ldc + coff[f], acc[k][f], false);
       }
     }
   } else {
@@ -317,18 +337,13 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
     for (int k = 0; k < V; ++k) {
       const int64_t row = (int64_t)panel * V + k;
       if (row < a.n_rows) {
-        T *crow = reinterpret_cast<T *>(a.C + row * a.ldc);
 #pragma unroll
         for (int f = 0; f < F; ++f)
-          if (cok[f]) {
-            if (sole)
-              st_c(crow + coff[f] / VW, acc[k][f], a.accumulate);
-            else
-              red_c(crow + coff[f] / VW, acc[k][f]);
-          }
+          if (cok[f]) put_c(a, row * a.ldc + coff[f], acc[k][f], !sole);
       }
     }
   }
+  if (a.fan.n) __threadfence_system();  // peers read after the caller's barrier
 }
 
 using KernelFn = void (*)(const SpmmArgs);

@@ -25,6 +25,7 @@ struct ShortArgs {
   int64_t ldb, ldc;
   int32_t row_begin, row_end, K;
   int32_t accumulate;  // 1: C += A.B
+  Fanout fan;          // peer copies of C (f2)
 };
 
 __device__ __forceinline__ int lda(const int32_t *p) {
@@ -136,6 +137,9 @@ __global__ void __launch_bounds__(256, 4) spmm_short_kernel(const ShortArgs a) {
           v.w += o.w;
         }
         __stcs(crow + f * G, v);
+#pragma unroll 1
+        for (int d = 0; d < a.fan.n; ++d)
+          __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + r * a.ldc + col0 + l * 4) + f * G, v);
       }
     h0 = h1;
     t0 = t1;
@@ -144,6 +148,7 @@ __global__ void __launch_bounds__(256, 4) spmm_short_kernel(const ShortArgs a) {
     c0 = c1;
     v0 = v1;
   }
+  if (a.fan.n) __threadfence_system();
 }
 
 using ShortFn = void (*)(const ShortArgs);
@@ -187,7 +192,7 @@ bool short_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc,
 
 pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
                             float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
-                            int64_t u0, int64_t u1, int32_t accumulate) {
+                            int64_t u0, int64_t u1, int32_t accumulate, const Fanout &fan) {
   if (u1 <= u0) return PSPMM_OK;
   const int F = cfg.F;
   int G = cfg.G ? cfg.G : ceil_pow2((K / 4 + F - 1) / F);
@@ -206,6 +211,7 @@ pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb
   args.row_end = (int32_t)u1;
   args.K = K;
   args.accumulate = accumulate;
+  args.fan = fan;
   const int threads = std::min(cfg.W, 8) * 32;
   const int64_t per_block = threads / 32 * (32 / G);
   // a few waves of resident blocks (256 x 4 launch bounds: 32 warps / SM)

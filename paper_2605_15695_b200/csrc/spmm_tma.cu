@@ -38,6 +38,7 @@ struct TmaArgs {
   int64_t ldc;
   int32_t n_rows, unit_begin, units, units_total, K;  // units = end of this launch's range
   int32_t accumulate;                                  // 1: C += A.B
+  Fanout fan;                                          // peer copies of C (f2)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -222,10 +223,19 @@ __global__ void __launch_bounds__(256, 1) spmm_tma_kernel(const __grid_constant_
           v.w += o.w;
         }
         __stcs(crow + q + f * 32, v);
-      } else
+#pragma unroll 1
+        for (int d = 0; d < a.fan.n; ++d)
+          __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + row * a.ldc + c0) + q + f * 32, v);
+      } else {
         atomicAdd(crow + q + f * 32, acc[k][f]);
+#pragma unroll 1
+        for (int d = 0; d < a.fan.n; ++d)
+          atomicAdd(reinterpret_cast<float4 *>(a.fan.peer[d] + row * a.ldc + c0) + q + f * 32,
+                    acc[k][f]);
+      }
     }
   }
+  if (a.fan.n) __threadfence_system();
 }
 
 using TmaFn = void (*)(const CUtensorMap, const TmaArgs);
@@ -274,7 +284,7 @@ bool tma_supported(int32_t K, int64_t ldb, int64_t ldc, const float *d_B, const 
 // Mode 2 dispatch (called from run_spmm after validation and the S = 1 zeroing).
 pspmm_status run_spmm_tma(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
                           float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
-                          int64_t u0, int64_t u1, int32_t accumulate) {
+                          int64_t u0, int64_t u1, int32_t accumulate, const Fanout &fan) {
   if (!tma_supported(K, ldb, ldc, d_B, d_C))
     PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run mode 2: unsupported K / layout");
   const int KP = tma_kp(K);
@@ -311,6 +321,7 @@ pspmm_status run_spmm_tma(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, 
   args.units_total = (int32_t)A->num_chunks;
   args.K = K;
   args.accumulate = accumulate;
+  args.fan = fan;
   if (u1 <= u0) return PSPMM_OK;
   const int64_t bx = (u1 - u0 + warps - 1) / warps;
   fn<<<dim3((unsigned)bx, (unsigned)passes), warps * 32, smem, stream>>>(map, args);

@@ -151,6 +151,109 @@ class ShardedSpmm:
         return self.C
 
 
+class FanoutSpmm:
+    """f2 (i): the all-gather fused into the SpMM epilogue.
+
+    Each rank holds two gathered buffers X[0], X[1] (P n_max x K each, one
+    allocation, double-buffered across layers).  A layer reads X[cur] and the
+    engine (pspmm_spmm_run_fanout) writes its output rows into slot `rank` of
+    X[1 - cur] on EVERY rank — its own copy plus P - 1 peer stores issued from
+    the epilogue as rows complete (NVLink P2P through CUDA-IPC mappings) — so
+    no collective follows the SpMM; a stream-ordered barrier (one-element
+    NCCL all-reduce) makes the peers' rows visible before the next layer.
+
+    connect(group) maps the peers' buffers (CUDA IPC, handles exchanged with
+    all_gather_object); connect_local(others) wires simulated ranks that live
+    in one process (single-GPU tests)."""
+
+    def __init__(self, shard: Shard, K: int, cfg: api.Config | None = None, device="cuda",
+                 stream=None):
+        import torch
+        self.shard = shard
+        self.K = K
+        self.cfg = cfg if cfg is not None else api.Config(W=4, F=1, V=1, S=1)
+        rp, ci, vl = shard.rowptr, shard.colidx, shard.val
+        self.A = _build((rp, ci if len(ci) else np.zeros(1, np.int32),
+                         vl if len(vl) else np.zeros(1, np.float32)),
+                        shard.rows, shard.n_cols, self.cfg, device, stream)
+        self.XX = torch.zeros((2, shard.n_cols, K), dtype=torch.float32, device=device)
+        self.X = [self.XX[0], self.XX[1]]
+        self.cur = 0
+        self.peers = [[], []]   # per buffer: device addresses of slot `rank` at each peer
+        self._opened = []
+        self._flag = None
+
+    @property
+    def slot_bytes(self) -> int:
+        return self.shard.rank * self.shard.n_max * self.K * 4
+
+    def own(self, b: int):
+        """This rank's rows of buffer b (a view; also what peers receive)."""
+        s = self.shard
+        return self.X[b][s.rank * s.n_max: s.rank * s.n_max + s.rows]
+
+    def connect(self, group=None):
+        import torch.distributed as dist
+        handle, off = api.pspmm_ipc_get_handle(self.XX)
+        world = dist.get_world_size(group)
+        allh = [None] * world
+        dist.all_gather_object(allh, (handle, off), group=group)
+        buf_bytes = self.shard.n_cols * self.K * 4
+        bases = {}
+        for q, (h, o) in enumerate(allh):
+            if q == self.shard.rank:
+                continue
+            if h not in bases:
+                bases[h] = api.pspmm_ipc_open(h)
+                self._opened.append(bases[h])
+            for b in (0, 1):
+                self.peers[b].append(bases[h] + o + b * buf_bytes + self.slot_bytes)
+
+    def connect_local(self, others):
+        """Simulated ranks in one process: others = the FanoutSpmm of every
+        other rank (same device)."""
+        for b in (0, 1):
+            self.peers[b] = [o.X[b].data_ptr() + self.slot_bytes for o in others]
+
+    def load(self, X_full):
+        """Initial layer input (the gathered B, P n_max x K) into X[cur]."""
+        self.X[self.cur].copy_(X_full)
+
+    def barrier(self, group=None):
+        import torch
+        import torch.distributed as dist
+        if dist.get_backend(group) == "nccl":
+            if self._flag is None:
+                self._flag = torch.zeros(1, dtype=torch.float32, device=self.XX.device)
+            dist.all_reduce(self._flag, group=group)  # stream-ordered
+        else:
+            torch.cuda.synchronize()
+            dist.barrier(group=group)
+
+    def step(self, stream=None, group=None, swap=True, barrier=True):
+        """One layer: own rows of X[1 - cur] (and their copies at every peer)
+        = A_shard . X[cur].  swap=False keeps reading X[0] (fixed-input
+        benchmarking).  Returns this rank's output rows."""
+        src, dst = self.cur, 1 - self.cur
+        out = self.own(dst)
+        api.pspmm_spmm_run_fanout(self.A, self.X[src], out, self.peers[dst], self.cfg, stream,
+                                  K=self.K)
+        if swap:
+            self.cur = dst
+        if barrier:
+            self.barrier(group)
+        return out
+
+    def close(self):
+        for b in self._opened:
+            try:
+                api.pspmm_ipc_close(b)
+            except Exception:
+                pass
+        self._opened = []
+        self.peers = [[], []]
+
+
 def split_own_columns(shard: Shard):
     """Local CSR split into (own, remote) column blocks, both canonical:
     own = columns owned by this rank, remapped to local row indices of B

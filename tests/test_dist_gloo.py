@@ -128,3 +128,56 @@ def test_two_rank_gloo_halo_exchange(name):
     if name == "roadnet":  # locality order: a thin halo at the shard boundary
         assert all(r[4] < 0.05 for r in res)
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _fanout_worker(rank, world, port, q):
+    """FanoutSpmm.connect's host logic with the CUDA IPC calls stubbed: the
+    handle exchange, one mapping per distinct peer allocation, and the peer
+    slot addresses (base + tensor offset + buffer b + this rank's slot)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import gen
+        from paper_2605_15695_b200 import api
+        from paper_2605_15695_b200 import dist as pdist
+        g = gen.config_graph("reddit", 0.002)
+        K = 8
+        sh = pdist.make_shard(g.rowptr, g.colidx, g.val, world, rank, align=2)
+        run = object.__new__(pdist.FanoutSpmm)
+        run.shard, run.K = sh, K
+        run.XX = torch.zeros((2, sh.n_cols, K))
+        run.peers, run._opened = [[], []], []
+        opened = []
+        api.pspmm_ipc_get_handle = lambda t: (bytes([65 + rank]) * 64, 4096 * (rank + 1))
+        api.pspmm_ipc_open = lambda h: opened.append(h) or (h[0] - 64) << 40
+        run.connect()
+        buf = sh.n_cols * K * 4
+        want = [[((q + 1) << 40) + 4096 * (q + 1) + b * buf + rank * sh.n_max * K * 4
+                 for q in range(world) if q != rank] for b in (0, 1)]
+        q.put(("ok", rank, run.peers == want, len(opened) == world - 1))
+    except Exception as e:  # pragma: no cover
+        q.put(("err", rank, repr(e), False))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_fanout_peer_addresses(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fanout_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    res = [q.get(timeout=5) for _ in range(world)]
+    for status, rank, ok_addr, ok_open in res:
+        assert status == "ok", ok_addr
+        assert ok_addr is True and ok_open is True
+    assert all(p.exitcode == 0 for p in procs)
