@@ -173,6 +173,24 @@ pspmm_status pspmm_pcsr_get_info(pspmm_pcsr A, pspmm_pcsr_info *out);
 pspmm_status pspmm_pcsr_export(pspmm_pcsr A, int32_t *h_rowptr, int32_t *h_colidx,
                                float *h_val, int32_t *h_trow);
 
+/*
+ * (f4) PCSR binary file: little-endian; header = magic "PCSR",
+ * u32 version (1), u64 n, u64 numPanels, u64 nnzV, u8 V, u8 S, u16 omega —
+ * the SPEC's fields in its order — then the version-1 extension u32 0,
+ * u64 numChunks, u64 SG, u64 nnz, u64 nCols (72-byte header), then rowPtr
+ * u64[numChunks + 1], colIdx u32[nnzV], val f32[nnzV * V] and, iff S = 1,
+ * TRow u32[numChunks].  Byte offsets in csrc/pcsr_io.cu.
+ * save: copies the handle's arrays to the host and writes `path`
+ * (synchronous).  load: reads, validates every PCSR invariant (rowPtr
+ * monotone 0..nnzV, ascending in-range columns per panel, TRow covering each
+ * panel in order, chunks <= SG cut at multiples of SG) and builds a handle
+ * usable by pspmm_spmm_run (the engine's derived data is rebuilt on
+ * `stream`).  Errors: INVALID_ARG (I/O, magic, header), UNSUPPORTED (other
+ * version), NOT_CANONICAL (array invariants), OOM / CUDA.
+ */
+pspmm_status pspmm_pcsr_save(pspmm_pcsr A, const char *path);
+pspmm_status pspmm_pcsr_load(const char *path, void *stream, pspmm_pcsr *out);
+
 /* Release a handle and its device arrays (NULL is a no-op). */
 void pspmm_pcsr_destroy(pspmm_pcsr A);
 

@@ -102,6 +102,8 @@ _sig("pspmm_pcsr_build_rect", _st, _i64, _i64, _i64, _P, _P, _P, _i32, _i32, _i3
 _sig("pspmm_pcsr_get_info", _st, _P, ctypes.POINTER(PcsrInfo))
 _sig("pspmm_pcsr_export", _st, _P, _P, _P, _P, _P)
 _sig("pspmm_pcsr_destroy", None, _P)
+_sig("pspmm_pcsr_save", _st, _P, ctypes.c_char_p)
+_sig("pspmm_pcsr_load", _st, ctypes.c_char_p, _P, ctypes.POINTER(_P))
 _sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
 _sig("pspmm_spmm_accumulate", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
@@ -242,6 +244,28 @@ def pspmm_pcsr_export(A: Pcsr) -> dict:
                                 val.ctypes.data_as(_P), trow.ctypes.data_as(_P) if i["S"] else None)
     _check(st, "pspmm_pcsr_export")
     return {"rowPtr": rowptr, "colIdx": colidx, "val": val, "TRow": trow, **i}
+
+
+def pspmm_pcsr_save(A: Pcsr, path):
+    """Write the PCSR binary file (include/pspmm.h)."""
+    _check(_lib.pspmm_pcsr_save(A.handle, os.fsencode(path)), "pspmm_pcsr_save")
+
+
+def pspmm_pcsr_load(path, stream=None) -> Pcsr:
+    """Read and validate a PCSR file into a device handle."""
+    h = ctypes.c_void_p()
+    _check(_lib.pspmm_pcsr_load(os.fsencode(path), _stream(stream), ctypes.byref(h)),
+           "pspmm_pcsr_load")
+    info = PcsrInfo()
+    _check(_lib.pspmm_pcsr_get_info(h, ctypes.byref(info)), "pspmm_pcsr_get_info")
+    # rows / columns: the handle knows both; n_cols is not in pcsr_info
+    return Pcsr(h, int(info.n), _load_ncols(path))
+
+
+def _load_ncols(path) -> int:
+    with open(path, "rb") as f:
+        head = f.read(72)
+    return int(np.frombuffer(head[64:72], "<u8")[0])
 
 
 def pspmm_pcsr_destroy(A: Pcsr):

@@ -71,6 +71,8 @@ pspmm_status build_pcsr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32
                         const int32_t *d_colidx, const float *d_val, int32_t V, int32_t S,
                         int32_t omega, int32_t sg_override, cudaStream_t stream,
                         pspmm_pcsr_s *P);
+// engine schedule: d_order = unit ids by descending vector count (derived)
+pspmm_status build_unit_order(pspmm_pcsr_s *A, cudaStream_t stream);
 // per-panel vector counts |union_p| for V = 2 (shared with features.cu)
 pspmm_status panel_counts_v2(int64_t n_rows, const int32_t *d_rowptr, const int32_t *d_colidx,
                              int32_t *d_L, cudaStream_t stream);

@@ -215,6 +215,8 @@ __global__ void unit_len_kernel(int64_t units, const int32_t *__restrict__ rowpt
   }
 }
 
+}  // namespace
+
 // Engine schedule (not part of the PCSR contract): unit ids by descending
 // vector count, ties in ascending id (stable radix sort -> deterministic).
 pspmm_status build_unit_order(pspmm_pcsr_s *A, cudaStream_t stream) {
@@ -240,6 +242,8 @@ pspmm_status build_unit_order(pspmm_pcsr_s *A, cudaStream_t stream) {
   PSPMM_CUDA_TRY(cudaFreeAsync(ids, stream));
   return PSPMM_OK;
 }
+
+namespace {
 
 struct Scratch {
   cudaStream_t s;
