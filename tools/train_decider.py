@@ -229,22 +229,26 @@ def emit_header(path, keys, model, source):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("inputs", nargs="+")
-    ap.add_argument("--depth", type=int, default=8)
+    ap.add_argument("--depth", type=int, default=10)
     ap.add_argument("--min-leaf", type=int, default=2)
-    ap.add_argument("--trees", type=int, default=48, help="forest size (1 = a single CART tree)")
-    ap.add_argument("--mtry", type=int, default=9, help="candidate features per split")
+    ap.add_argument("--trees", type=int, default=96, help="forest size (1 = a single CART tree)")
+    ap.add_argument("--mtry", type=int, default=12, help="candidate features per split")
     ap.add_argument("--out-header", default=os.path.join(ROOT, "paper_2605_15695_b200", "csrc",
                                                          "decider_model.h"))
     ap.add_argument("--eval-json", default=None)
+    ap.add_argument("--split-seed", type=int, default=2605,
+                    help="seed of the 80/20 graph split (hyper-parameters are chosen on the "
+                         "mean over several split seeds, DESIGN.md §6)")
     a = ap.parse_args()
     recs = load(a.inputs)
     keys, X, perf = build_matrix(recs)
     graphs = sorted({r["graph"] for r in recs})
-    rng = np.random.default_rng(2605)
+    rng = np.random.default_rng(a.split_seed)
     test_graphs = set(rng.choice(graphs, size=max(1, len(graphs) // 5), replace=False).tolist())
     tr = [i for i, r in enumerate(recs) if r["graph"] not in test_graphs]
     te = [i for i, r in enumerate(recs) if r["graph"] in test_graphs]
     report = {"records": len(recs), "graphs": len(graphs), "labels": len(keys),
+              "split_seed": a.split_seed,
               "test_graphs": sorted(test_graphs),
               "protocol": "80/20 split by graph (P:399); normalized performance = t_best / t; "
                           "rnd = a uniformly random valid lattice config; rule = the untrained "
