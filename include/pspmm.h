@@ -73,6 +73,9 @@ typedef enum {
  *     aligned B and C, else PSPMM_ERR_UNSUPPORTED; only W applies);
  *     3 = short-row pipeline for low-degree graphs (V = 1, S = 0, F in
  *     {1, 2, 4}, 128-bit layout; W, F, G apply);
+ *     4 = short-row stream with cp.async shared-memory rings: a row group
+ *     owns a contiguous row range and streams its vectors, B rows of 3
+ *     batches ahead in flight (same constraints as 3; W, F, G apply);
  *     1 is reserved for a dense-panel tensor-core path and returns
  *     PSPMM_ERR_UNSUPPORTED.
  *  order  mode 0 only: 1 = visit units by descending vector count (a

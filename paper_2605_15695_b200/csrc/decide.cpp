@@ -86,7 +86,7 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
   c.W = lab[3];
   c.order = c.mode == 0 ? lab[6] : 0;
   if (c.mode == 2 && K % 32 != 0) c.mode = 0;  // TMA engine needs K % 32 == 0
-  if (c.mode == 3 && K % 4 != 0) c.mode = 0;   // short-row engine is 128-bit only
+  if ((c.mode == 3 || c.mode == 4) && K % 4 != 0) c.mode = 0;  // short-row engines: 128-bit only
   if (c.mode == 2) {
     pick_fg(K, 0, &c.F, &c.G);  // unused by mode 2; a valid mode-0 fallback
   } else if (lab[0] == 2) {

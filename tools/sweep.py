@@ -92,12 +92,13 @@ def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2,
             if 2 in modes and K % 32 == 0:  # TMA gather engine: only W matters
                 points += [(2, W, 0, 0, 0) for W in (1, 2, 4, 8)
                            if W * 8 * 16 * min(K, 256) <= 227 * 1024]
-            if 3 in modes and V == 1 and S == 0 and K % 4 == 0:  # short-row engine
-                for F in (1, 2, 4):
-                    G = 1
-                    while G < -(-(K // 4) // F) and G < 32:
-                        G <<= 1
-                    points += [(3, W, F, max(G, 2), 0) for W in (2, 4, 8)]
+            for m in (3, 4):  # short-row engines
+                if m in modes and V == 1 and S == 0 and K % 4 == 0:
+                    for F in (1, 2, 4):
+                        G = 1
+                        while G < -(-(K // 4) // F) and G < 32:
+                            G <<= 1
+                        points += [(m, W, F, max(G, 2), 0) for W in (2, 4, 8)]
             for (mode, W, F, G, order) in points:
                 cfg = api.Config(W=W, F=max(F, 1), V=V, S=S, G=G, mode=mode, order=order)
                 evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
