@@ -75,7 +75,7 @@ def test_c_decider_evaluates_the_header_tree():
         if mode == 2 and K % 32 == 0:
             assert (c.mode, c.V, c.S, c.W) == (2, V, S, W)
         elif mode in (3, 4) and K % 4 == 0:
-            assert (c.mode, c.V, c.S, c.W, c.F) == (3, V, S, W, F)
+            assert (c.mode, c.V, c.S, c.W, c.F) == (mode, V, S, W, F)
         else:
             assert (c.mode, c.V, c.S, c.W) == (0, V, S, W)
             if mode == 0:
