@@ -58,6 +58,18 @@ if want sweep_order; then
   timeout 2400 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --Ws 2,4 \
       --orders 1 --out $O/sweep_corpus_o1.json > $O/sweep_corpus_o1.log 2>&1
 fi
+if want tests4; then
+  timeout 1800 python -m pytest tests -m gpu -q -k "short or async or fanout or accumulate or cli" \
+      --maxfail=10 > $O/pytest_gpu4.log 2>&1
+  echo "pytest exit $?" >> $O/pytest_gpu4.log
+fi
+if want sweep4; then
+  # engine mode 4 (V = 1, S = 0 only), merged by (graph, K) like mode 3
+  timeout 900 python tools/sweep.py --workloads cora,roadnet,reddit,proteins,products --iters 5 \
+      --VS 10 --modes 3,4 --out $O/sweep_workloads_m4.json > $O/sweep_workloads_m4.log 2>&1
+  timeout 1800 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --VS 10 \
+      --modes 4 --out $O/sweep_corpus_m4.json > $O/sweep_corpus_m4.log 2>&1
+fi
 # never let gpurun_out/ exceed the 64 MiB merge limit
 if [ "$(du -sm $O | cut -f1)" -gt 56 ]; then rm -f $O/*.ncu-rep; fi
 echo done > $O/round_done.txt
