@@ -70,6 +70,11 @@ if want sweep4; then
   timeout 1800 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --VS 10 \
       --modes 4 --out $O/sweep_corpus_m4.json > $O/sweep_corpus_m4.log 2>&1
 fi
+if want diag; then
+  for w in reddit products; do
+    timeout 600 python tools/e2e_diag.py --workload $w > $O/e2e_diag_$w.json 2> $O/e2e_diag_$w.log
+  done
+fi
 # never let gpurun_out/ exceed the 64 MiB merge limit
 if [ "$(du -sm $O | cut -f1)" -gt 56 ]; then rm -f $O/*.ncu-rep; fi
 echo done > $O/round_done.txt
