@@ -236,6 +236,24 @@ pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, in
                                  float *d_Cbuf, void *stream);
 
 /*
+ * Host batch entry (serving / a stream of feature matrices through one A):
+ * count independent products C_i = A . B_i with host-resident h_B[i]
+ * (n_cols x K, ldb) and h_C[i] (n x K, ldc), host ARRAYS of count host
+ * pointers each.  Two caller-owned device buffer sets d_B[0..1] / d_C[0..1]
+ * (host arrays of 2 device pointers, same layouts) rotate, so the H2D copy
+ * of B_{i+1} and the D2H copy of C_{i-1} run on internal copy streams while
+ * the engine computes product i on `stream` (whole matrix, unit order
+ * honoured).  Synchronises `stream` at the end.  h_B / h_C should be pinned.
+ * The first call on a handle creates its copy streams and events (released
+ * by destroy).  Errors as pspmm_spmm_run, plus INVALID_ARG for null
+ * pointers or count < 0.
+ */
+pspmm_status pspmm_spmm_run_host_batch(pspmm_pcsr A, const float *const *h_B, int64_t ldb,
+                                       int32_t K, float *const *h_C, int64_t ldc, int32_t count,
+                                       pspmm_config cfg, float *const *d_B, float *const *d_C,
+                                       void *stream);
+
+/*
  * (f2 (i): the all-gather fused into the SpMM epilogue)
  * C = A . B exactly as pspmm_spmm_run, and every C element the engine writes
  * (stores, split-panel atomics, the zeroing of split rows) is also written at

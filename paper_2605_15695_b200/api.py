@@ -107,6 +107,7 @@ _sig("pspmm_pcsr_load", _st, ctypes.c_char_p, _P, ctypes.POINTER(_P))
 _sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
 _sig("pspmm_spmm_accumulate", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
+_sig("pspmm_spmm_run_host_batch", _st, _P, _P, _i64, _i32, _P, _i64, _i32, Config, _P, _P, _P)
 _sig("pspmm_spmm_run_fanout", _st, _P, _P, _i64, _i32, _P, _i64, _P, _i32, Config, _P)
 _sig("pspmm_ipc_get_handle", _st, _P, _P, ctypes.POINTER(_i64))
 _sig("pspmm_ipc_open", _st, _P, ctypes.POINTER(_P))
@@ -291,6 +292,41 @@ def pspmm_spmm_accumulate(A: Pcsr, B, C, cfg: Config, stream=None, K=None):
         raise ValueError("B / C shapes do not match the PCSR handle and K")
     _check(_lib.pspmm_spmm_accumulate(A.handle, b, ldb, K, c, ldc, cfg, _stream(stream)),
            "pspmm_spmm_accumulate")
+
+
+def pspmm_spmm_run_host_batch(A: Pcsr, hBs, hCs, cfg: Config, dBs, dCs, stream=None):
+    """C_i = A . B_i for pinned host tensors hBs[i] -> hCs[i] (same shapes),
+    two device buffer sets dBs[0..1] / dCs[0..1] rotating so copies overlap
+    the engine.  Synchronous."""
+    torch = _torch()
+    if len(hBs) != len(hCs) or len(dBs) != 2 or len(dCs) != 2:
+        raise ValueError("need as many outputs as inputs and two device buffer sets")
+    K = None
+    hb, hc = [], []
+    for b, c in zip(hBs, hCs):
+        for t in (b, c):
+            if not (isinstance(t, torch.Tensor) and t.device.type == "cpu" and
+                    t.dtype == torch.float32 and t.is_contiguous()):
+                raise TypeError("host matrices must be contiguous float32 CPU tensors")
+        if K is None:
+            K = b.shape[1]
+        if b.shape[1] != K or c.shape[1] != K:
+            raise ValueError("every B_i / C_i must have K columns")
+        hb.append(b.data_ptr())
+        hc.append(c.data_ptr())
+    db = [_dense(t, "dB") for t in dBs]
+    dc = [_dense(t, "dC") for t in dCs]
+    if K is None:
+        return
+    if db[0][1] != db[1][1] or dc[0][1] != dc[1][1] or db[0][1] != K or dc[0][1] != K:
+        raise ValueError("device buffers must be contiguous n x K like the host matrices")
+    n = len(hb)
+    HB = (ctypes.c_void_p * n)(*hb)
+    HC = (ctypes.c_void_p * n)(*hc)
+    DB = (ctypes.c_void_p * 2)(db[0][0].value, db[1][0].value)
+    DC = (ctypes.c_void_p * 2)(dc[0][0].value, dc[1][0].value)
+    _check(_lib.pspmm_spmm_run_host_batch(A.handle, HB, K, K, HC, K, n, cfg, DB, DC,
+                                          _stream(stream)), "pspmm_spmm_run_host_batch")
 
 
 MAX_PEERS = 7  # PSPMM_MAX_PEERS

@@ -160,6 +160,15 @@ void pspmm_pcsr_destroy(pspmm_pcsr A) {
     for (int k = 0; k < kSlices; ++k)
       if (A->slice_done[k]) cudaEventDestroy(A->slice_done[k]);
   }
+  for (cudaStream_t s : {A->h2d_stream, A->d2h_stream})
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  for (int b = 0; b < 2; ++b)
+    for (cudaEvent_t e : {A->h2d_done[b], A->comp_done[b], A->d2h_done[b]})
+      if (e) cudaEventDestroy(e);
+  if (A->batch_start) cudaEventDestroy(A->batch_start);
   delete A;
 }
 
@@ -239,6 +248,31 @@ pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, in
     return PSPMM_ERR_DIM_MISMATCH;
   }
   return run_spmm_host(A, h_B, ldb, K, h_C, ldc, cfg, d_Bbuf, d_Cbuf, as_stream(stream));
+}
+
+pspmm_status pspmm_spmm_run_host_batch(pspmm_pcsr A, const float *const *h_B, int64_t ldb,
+                                       int32_t K, float *const *h_C, int64_t ldc, int32_t count,
+                                       pspmm_config cfg, float *const *d_B, float *const *d_C,
+                                       void *stream) {
+  if (!A || !h_B || !h_C || !d_B || !d_C || count < 0) {
+    set_error("spmm_run_host_batch: null argument or negative count");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  for (int32_t i = 0; i < count; ++i)
+    if (!h_B[i] || !h_C[i]) {
+      set_error("spmm_run_host_batch: null host matrix");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+  for (int b = 0; b < 2; ++b)
+    if (!d_B[b] || !d_C[b]) {
+      set_error("spmm_run_host_batch: null device buffer");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+  if (K < 1 || ldb < K || ldc < K) {
+    set_error("spmm_run_host_batch: need K >= 1, ldb >= K, ldc >= K");
+    return PSPMM_ERR_DIM_MISMATCH;
+  }
+  return run_spmm_host_batch(A, h_B, ldb, K, h_C, ldc, count, cfg, d_B, d_C, as_stream(stream));
 }
 
 pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,

@@ -30,6 +30,10 @@ struct pspmm_pcsr_s {
   int64_t slice_rows[kSlices + 1] = {};
   cudaStream_t copy_stream = nullptr;  // created lazily by pspmm_spmm_run_host
   cudaEvent_t slice_done[kSlices] = {};
+  int64_t max_unit_len = 0;            // vectors of the longest unit (load-balance check)
+  // pspmm_spmm_run_host_batch: copy-in / copy-out streams and per-buffer events
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {}, batch_start = nullptr;
 };
 
 namespace pspmm {
@@ -114,6 +118,12 @@ pspmm_status run_spmm_async(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb
 pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32_t K, float *h_C,
                            int64_t ldc, const pspmm_config &cfg, float *d_Bbuf, float *d_Cbuf,
                            cudaStream_t stream);
+// host batch entry: count independent B -> C products through two device
+// buffer sets, H2D of i + 1 and D2H of i - 1 overlapping the engine on i
+pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64_t ldb, int32_t K,
+                                 float *const *h_C, int64_t ldc, int32_t count,
+                                 const pspmm_config &cfg, float *const *d_B, float *const *d_C,
+                                 cudaStream_t stream);
 
 // transpose.cu (f3: backward SpMM operand)
 pspmm_status csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t *d_rowptr,

@@ -237,6 +237,12 @@ pspmm_status build_unit_order(pspmm_pcsr_s *A, cudaStream_t stream) {
   PSPMM_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, len, len_sorted, ids,
                                                            A->d_order, (int)units, 0, 32, stream));
   PSPMM_CUDA_TRY(cudaFreeAsync(tmp, stream));
+  // the longest unit's vector count (its id leads the order)
+  int32_t lmax = 0;
+  PSPMM_CUDA_TRY(cudaMemcpyAsync(&lmax, len_sorted, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                 stream));
+  PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
+  A->max_unit_len = lmax;
   PSPMM_CUDA_TRY(cudaFreeAsync(len, stream));
   PSPMM_CUDA_TRY(cudaFreeAsync(len_sorted, stream));
   PSPMM_CUDA_TRY(cudaFreeAsync(ids, stream));

@@ -215,6 +215,21 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
                       f);
 }
 
+namespace {
+
+// Slicing the engine into kSlices unit ranges overlaps the D2H copy with the
+// compute, but each slice lasts at least as long as its longest unit (one
+// row group works through it).  When the longest unit holds more vectors
+// than a slice's fair share per resident row group, slices would serialise
+// on their hub rows: run the engine whole (with its unit order) instead.
+bool slices_balanced(const pspmm_pcsr_s *A, const Plan &plan) {
+  const int64_t groups = (int64_t)num_sms() * (PSPMM_MAX_THREADS * PSPMM_MIN_BLOCKS / 32) *
+                         (32 / std::max(1, plan.G));
+  return A->max_unit_len * kSlices * groups <= A->nnz_v;
+}
+
+}  // namespace
+
 pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32_t K, float *h_C,
                            int64_t ldc, const pspmm_config &cfg, float *d_Bbuf, float *d_Cbuf,
                            cudaStream_t stream) {
@@ -223,6 +238,20 @@ pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32
   Plan plan;
   pspmm_status st = make_plan(A, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, &plan);
   if (st != PSPMM_OK) return st;
+  const Fanout none{};
+  if (cfg.mode == 0 && !slices_balanced(A, plan)) {
+    PSPMM_CUDA_TRY(cudaMemcpyAsync(d_Bbuf, h_B, (size_t)A->n_cols * ldb * sizeof(float),
+                                   cudaMemcpyHostToDevice, stream));
+    st = prepare_c(A, K, d_Cbuf, ldc, stream, none);
+    if (st != PSPMM_OK) return st;
+    st = launch_range(A, plan, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, stream, 0, A->num_chunks, 0,
+                      none);
+    if (st != PSPMM_OK) return st;
+    PSPMM_CUDA_TRY(cudaMemcpyAsync(h_C, d_Cbuf, (size_t)A->n_rows * ldc * sizeof(float),
+                                   cudaMemcpyDeviceToHost, stream));
+    PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
+    return PSPMM_OK;
+  }
   if (!A->copy_stream) {
     PSPMM_CUDA_TRY(cudaStreamCreateWithFlags(&A->copy_stream, cudaStreamNonBlocking));
     for (int k = 0; k < kSlices; ++k)
@@ -230,7 +259,6 @@ pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32
   }
   PSPMM_CUDA_TRY(cudaMemcpyAsync(d_Bbuf, h_B, (size_t)A->n_cols * ldb * sizeof(float),
                                  cudaMemcpyHostToDevice, stream));
-  const Fanout none{};
   st = prepare_c(A, K, d_Cbuf, ldc, stream, none);
   if (st != PSPMM_OK) return st;
   for (int k = 0; k < kSlices; ++k) {
@@ -248,6 +276,58 @@ pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32
   // the caller's stream observes the copies' completion, then the host waits
   PSPMM_CUDA_TRY(cudaEventRecord(A->slice_done[0], A->copy_stream));
   PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->slice_done[0], 0));
+  PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
+  return PSPMM_OK;
+}
+
+pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64_t ldb, int32_t K,
+                                 float *const *h_C, int64_t ldc, int32_t count,
+                                 const pspmm_config &cfg, float *const *d_B, float *const *d_C,
+                                 cudaStream_t stream) {
+  Plan plan[2];
+  for (int b = 0; b < 2; ++b) {
+    pspmm_status st = make_plan(A, d_B[b], ldb, K, d_C[b], ldc, cfg, &plan[b]);
+    if (st != PSPMM_OK) return st;
+  }
+  if (!A->h2d_stream) {
+    PSPMM_CUDA_TRY(cudaStreamCreateWithFlags(&A->h2d_stream, cudaStreamNonBlocking));
+    PSPMM_CUDA_TRY(cudaStreamCreateWithFlags(&A->d2h_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      PSPMM_CUDA_TRY(cudaEventCreateWithFlags(&A->h2d_done[b], cudaEventDisableTiming));
+      PSPMM_CUDA_TRY(cudaEventCreateWithFlags(&A->comp_done[b], cudaEventDisableTiming));
+      PSPMM_CUDA_TRY(cudaEventCreateWithFlags(&A->d2h_done[b], cudaEventDisableTiming));
+    }
+    PSPMM_CUDA_TRY(cudaEventCreateWithFlags(&A->batch_start, cudaEventDisableTiming));
+  }
+  // the copy streams start after the work already queued on `stream`
+  PSPMM_CUDA_TRY(cudaEventRecord(A->batch_start, stream));
+  PSPMM_CUDA_TRY(cudaStreamWaitEvent(A->h2d_stream, A->batch_start, 0));
+  PSPMM_CUDA_TRY(cudaStreamWaitEvent(A->d2h_stream, A->batch_start, 0));
+  const Fanout none{};
+  const size_t b_bytes = (size_t)A->n_cols * ldb * sizeof(float);
+  const size_t c_bytes = (size_t)A->n_rows * ldc * sizeof(float);
+  for (int32_t i = 0; i < count; ++i) {
+    const int b = i & 1;
+    // buffer set b is free once product i - 2 has been computed / copied out
+    if (i >= 2) PSPMM_CUDA_TRY(cudaStreamWaitEvent(A->h2d_stream, A->comp_done[b], 0));
+    PSPMM_CUDA_TRY(cudaMemcpyAsync(d_B[b], h_B[i], b_bytes, cudaMemcpyHostToDevice,
+                                   A->h2d_stream));
+    PSPMM_CUDA_TRY(cudaEventRecord(A->h2d_done[b], A->h2d_stream));
+    PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->h2d_done[b], 0));
+    if (i >= 2) PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->d2h_done[b], 0));
+    pspmm_status st = prepare_c(A, K, d_C[b], ldc, stream, none);
+    if (st != PSPMM_OK) return st;
+    st = launch_range(A, plan[b], d_B[b], ldb, K, d_C[b], ldc, cfg, stream, 0, A->num_chunks, 0,
+                      none);
+    if (st != PSPMM_OK) return st;
+    PSPMM_CUDA_TRY(cudaEventRecord(A->comp_done[b], stream));
+    PSPMM_CUDA_TRY(cudaStreamWaitEvent(A->d2h_stream, A->comp_done[b], 0));
+    PSPMM_CUDA_TRY(cudaMemcpyAsync(h_C[i], d_C[b], c_bytes, cudaMemcpyDeviceToHost,
+                                   A->d2h_stream));
+    PSPMM_CUDA_TRY(cudaEventRecord(A->d2h_done[b], A->d2h_stream));
+  }
+  for (int b = 0; b < 2 && b < count; ++b)
+    PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->d2h_done[b], 0));
   PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
   return PSPMM_OK;
 }

@@ -62,8 +62,9 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 template <int F, int G>
-constexpr int warp_bytes() {
-  return kRB * kU * F * 32 * 16 + (32 / G) * kRC * kU * 8 + (32 / G) * 2 * (kSub + 1) * 4;
+constexpr int warp_bytes() {  // rounded to 16 B: every warp's B ring stays 16-B aligned
+  return (kRB * kU * F * 32 * 16 + (32 / G) * kRC * kU * 8 + (32 / G) * 2 * (kSub + 1) * 4 + 15) /
+         16 * 16;
 }
 
 template <int F, int G>

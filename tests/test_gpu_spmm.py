@@ -305,6 +305,35 @@ def test_host_e2e_entry(V, S, mode):
         assert_parity(hC.numpy(), ref, mag, f"host e2e V{V} S{S} mode{mode}")
 
 
+@pytest.mark.parametrize("name,V,S,mode,order", [
+    ("products_s", 1, 1, 0, 0), ("products_s", 2, 0, 0, 1), ("giant", 1, 0, 0, 1),
+    ("roadnet_s", 1, 0, 3, 0), ("roadnet_s", 1, 0, 4, 0), ("reddit_s", 1, 1, 2, 0)])
+def test_host_entries_whole_and_batch(name, V, S, mode, order):
+    """pspmm_spmm_run_host on skewed S = 0 handles (hub rows: the whole-matrix
+    path) and pspmm_spmm_run_host_batch (two rotating buffer sets, copies on
+    internal streams): every product of the batch matches the oracle."""
+    api, torch = _api(), _torch()
+    g = graph(name)
+    K = 64
+    rp, ci, vl = dev(g)
+    cfg = api.Config(V=V, S=S, F=1, W=4, mode=mode, order=order)
+    A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, V, S)
+    Bs = [gen.dense(g.n, K, 700 + i) for i in range(5)]
+    refs = [oracle_ref(g, B) for B in Bs]
+    hB = [torch.from_numpy(B).pin_memory() for B in Bs]
+    hC = [torch.full((g.n, K), float("nan")).pin_memory() for _ in Bs]
+    dB = [torch.empty((g.n, K), device="cuda") for _ in range(2)]
+    dC = [torch.empty((g.n, K), device="cuda") for _ in range(2)]
+    api.pspmm_spmm_run_host(A, hB[0], hC[0], cfg, dB[0], dC[0])
+    assert_parity(hC[0].numpy(), *refs[0], f"host {name} V{V} S{S} m{mode}")
+    for count in (5, 1, 0, 5):  # reuse of the handle's streams / events
+        for c in hC:
+            c.fill_(float("nan"))
+        api.pspmm_spmm_run_host_batch(A, hB[:count], hC[:count], cfg, dB, dC)
+        for i in range(count):
+            assert_parity(hC[i].numpy(), *refs[i], f"batch {i}/{count} {name} m{mode}")
+
+
 def test_graph_capture_and_streams():
     """spmm_run allocates nothing, so it can be captured in a CUDA graph and
     replayed on a side stream."""

@@ -59,7 +59,7 @@ if want sweep_order; then
       --orders 1 --out $O/sweep_corpus_o1.json > $O/sweep_corpus_o1.log 2>&1
 fi
 if want tests4; then
-  timeout 1800 python -m pytest tests -m gpu -q -k "short or async or fanout or accumulate or cli" \
+  timeout 1800 python -m pytest tests -m gpu -q -k "short or async or fanout or accumulate or cli or host" \
       --maxfail=10 > $O/pytest_gpu4.log 2>&1
   echo "pytest exit $?" >> $O/pytest_gpu4.log
 fi
@@ -69,6 +69,10 @@ if want sweep4; then
       --VS 10 --modes 3,4 --out $O/sweep_workloads_m4.json > $O/sweep_workloads_m4.log 2>&1
   timeout 1800 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --VS 10 \
       --modes 4 --out $O/sweep_corpus_m4.json > $O/sweep_corpus_m4.log 2>&1
+fi
+if want quickbench; then
+  timeout 900 python bench.py --headline-only > $O/bench_quick.log 2>&1
+  echo "bench exit $?" >> $O/bench_quick.log
 fi
 if want diag; then
   for w in reddit products; do
