@@ -500,7 +500,9 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
     (frac,) = max_over_ranks([pdist.halo_fraction(g.rowptr, g.colidx, bounds, rank)])
     use_halo = args.exchange == "halo" or (args.exchange == "auto" and frac < 0.5)
     fanout, fanout_note = None, None
-    if not use_halo and args.exchange in ("auto", "fanout") and args.dist_backend == "nccl":
+    # (gloo: the single-GPU rehearsal of the flow, --exchange fanout only)
+    if not use_halo and (args.exchange == "fanout" or
+                         (args.exchange == "auto" and args.dist_backend == "nccl")):
         fanout, fanout_note = setup_fanout(g, cfg, gen.config_B(g.name, g.n), world, rank,
                                            stream)
 

@@ -74,6 +74,15 @@ if want quickbench; then
   timeout 900 python bench.py --headline-only > $O/bench_quick.log 2>&1
   echo "bench exit $?" >> $O/bench_quick.log
 fi
+if want rehearse; then
+  # the N > 1 bench flow on one GPU: 2 processes, gloo, every exchange
+  for ex in fanout allgather halo; do
+    timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+        --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 4 --warmup 3 \
+        --dist-backend gloo --exchange $ex --workload reddit > $O/rehearse_$ex.log 2>&1
+    echo "exit $?" >> $O/rehearse_$ex.log
+  done
+fi
 if want diag; then
   for w in reddit products; do
     timeout 600 python tools/e2e_diag.py --workload $w > $O/e2e_diag_$w.json 2> $O/e2e_diag_$w.log
