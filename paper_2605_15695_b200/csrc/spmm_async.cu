@@ -25,8 +25,14 @@
 namespace pspmm {
 namespace {
 
-constexpr int kU = 4;         // vectors per batch
-constexpr int kD = 3;         // batches of B rows in flight
+#ifndef PSPMM_ASYNC_U
+#define PSPMM_ASYNC_U 4
+#endif
+#ifndef PSPMM_ASYNC_D
+#define PSPMM_ASYNC_D 3
+#endif
+constexpr int kU = PSPMM_ASYNC_U;  // vectors per batch
+constexpr int kD = PSPMM_ASYNC_D;  // batches of B rows in flight
 constexpr int kRC = 2 * kD + 1;  // (colIdx, val) ring slots: batches b .. b + 2D
 constexpr int kRB = kD + 1;      // B ring slots: batches b .. b + D
 constexpr int kSub = 32;         // rows per staged rowPtr sub-tile

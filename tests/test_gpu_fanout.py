@@ -76,7 +76,10 @@ def test_fanout_simulated_ranks(P, mode, V, S):
         assert run.cur == 0
         for q, s in enumerate(shards):
             got = run.X[0][q * n_max: q * n_max + s.rows]
-            torch.testing.assert_close(got, plain[q], rtol=1e-5, atol=1e-5)
+            # S = 1 atomics sum in a run-dependent order: tolerance relative
+            # to the layer-2 magnitudes
+            torch.testing.assert_close(got, plain[q], rtol=1e-4,
+                                       atol=1e-5 * float(plain[q].abs().max()))
 
 
 def test_fanout_argument_errors():

@@ -139,7 +139,11 @@ def test_short_row_engines(mode, name, K, F):
     B = gen.dense(g.n, K, 500 + K)
     ref, mag = oracle_ref(g, B, key=(name, K, "short"))
     for W in (2, 8):
-        C, _ = run(g, B, api.Config(W=W, F=F, V=1, S=0, mode=mode))
+        try:
+            C, _ = run(g, B, api.Config(W=W, F=F, V=1, S=0, mode=mode))
+        except api.PspmmError as e:  # mode 4: W warps' rings exceed shared memory
+            assert mode == 4 and F == 4 and W == 8 and e.status == api.PSPMM_ERR_CONFIG
+            continue
         assert_parity(C, ref, mag, f"mode {mode} {name} K{K} F{F} W{W}")
 
 

@@ -83,6 +83,23 @@ if want rehearse; then
     echo "exit $?" >> $O/rehearse_$ex.log
   done
 fi
+if want async_ab; then
+  for v in main ad2 ad6 au8 ad6u8; do
+    if [ "$v" = main ]; then unset PSPMM_LIB; M=3,4; else export PSPMM_LIB=$PWD/paper_2605_15695_b200/variants/libpspmm_$v.so; M=4; fi
+    timeout 600 python tools/sweep.py --workloads roadnet,cora --VS 10 --modes $M --Ws 2,4,8 --iters 7 \
+        --out $O/async_$v.json > $O/async_$v.log 2>&1
+  done
+  unset PSPMM_LIB
+  for m in 3 4; do
+    if [ $m = 3 ]; then X="--W 2 --F 2 --G 4"; else X="--W 8 --F 1 --G 8"; fi
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm -s 1 -c 1 \
+        -o /tmp/prof_rn_m$m -f python tools/run_kernel.py --workload roadnet --iters 2 --V 1 --S 0 \
+        --mode $m $X > $O/ncu_rn_m$m.log 2>&1
+    python tools/ncu_summary.py /tmp/prof_rn_m$m.ncu-rep --json $O/ncu_rn_m$m.json > /dev/null 2>&1
+    ncu -i /tmp/prof_rn_m$m.ncu-rep --page source --csv > $O/ncu_rn_m${m}_source.csv 2>/dev/null
+    ncu -i /tmp/prof_rn_m$m.ncu-rep --page details --csv > $O/ncu_rn_m${m}_details.csv 2>/dev/null
+  done
+fi
 if want diag; then
   for w in reddit products; do
     timeout 600 python tools/e2e_diag.py --workload $w > $O/e2e_diag_$w.json 2> $O/e2e_diag_$w.log

@@ -19,7 +19,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="reddit")
     ap.add_argument("--iters", type=int, default=3)
-    for k in ("V", "S", "F", "G", "W", "sg"):
+    for k in ("V", "S", "F", "G", "W", "sg", "mode", "order"):
         ap.add_argument(f"--{k}", type=int, default=None)
     a = ap.parse_args()
     g = bench.load_graph(a.workload)
@@ -27,7 +27,7 @@ def main():
     ci = torch.from_numpy(g.colidx).cuda()
     vl = torch.from_numpy(g.val).cuda()
     cfg = api.auto_config(g.n, g.nnz, rp, ci, g.K)
-    for k in ("V", "S", "F", "G", "W"):
+    for k in ("V", "S", "F", "G", "W", "mode", "order"):
         if getattr(a, k) is not None:
             setattr(cfg, k, getattr(a, k))
     if a.sg is not None:
