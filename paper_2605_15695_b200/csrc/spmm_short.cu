@@ -40,8 +40,17 @@ __device__ __forceinline__ float lda(const float *p) {
 }
 
 template <int F, int G>
-__global__ void __launch_bounds__(256, 4) spmm_short_kernel(const ShortArgs a) {
-  constexpr int UNR = 4;  // vectors of a row whose B rows are in flight together
+#ifndef PSPMM_SHORT_MINB
+#define PSPMM_SHORT_MINB 4  // resident 256-thread blocks per SM (register budget)
+#endif
+#ifndef PSPMM_SHORT_UNR
+#define PSPMM_SHORT_UNR 4
+#endif
+#ifndef PSPMM_SHORT_WAVES
+#define PSPMM_SHORT_WAVES 2
+#endif
+__global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const ShortArgs a) {
+  constexpr int UNR = PSPMM_SHORT_UNR;  // vectors of a row whose B rows are in flight together
   const int lane = threadIdx.x & 31;
   const int g = lane / G, l = lane % G;
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
@@ -214,10 +223,10 @@ pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb
   args.fan = fan;
   const int threads = std::min(cfg.W, 8) * 32;
   const int64_t per_block = threads / 32 * (32 / G);
-  // a few waves of resident blocks (256 x 4 launch bounds: 32 warps / SM)
-  const int64_t resident = std::max<int64_t>(1, 1024 / threads);
+  // a few waves of resident blocks (launch bounds: 256 x PSPMM_SHORT_MINB threads / SM)
+  const int64_t resident = std::max<int64_t>(1, 256 * PSPMM_SHORT_MINB / threads);
   int64_t bx = (u1 - u0 + per_block - 1) / per_block;
-  bx = std::min<int64_t>(bx, (int64_t)num_sms() * resident * 2);
+  bx = std::min<int64_t>(bx, (int64_t)num_sms() * resident * PSPMM_SHORT_WAVES);
   const int64_t by = (K + 4 * G * F - 1) / (4 * G * F);
   fn<<<dim3((unsigned)bx, (unsigned)by), threads, 0, stream>>>(args);
   PSPMM_CUDA_TRY(cudaGetLastError());
