@@ -135,6 +135,25 @@ def workload_desc(g):
     return f"{g.name}-shaped synthetic graph (n={g.n}, nnz={g.nnz}, K={g.K})"
 
 
+def gather_roofline(name, head, K, ms):
+    """The binding on-chip limit of the high-degree configs: B-row bytes
+    gathered per launch (nnz_V vectors x K x 4; each vector fetches its B row
+    once) against the measured bare-gather ceiling of the same pattern on
+    this B200 (profiles/gather_ceiling.json, tools/microbench_gather.cu)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_ceiling.json")) as f:
+            ceil = json.load(f).get(name)
+        nnz_v = head["pcsr"]["nnz_v"]
+    except Exception:
+        return None
+    if not ceil:
+        return None
+    gathered = nnz_v * K * 4
+    tbps = gathered / (ms * 1e-3) / 1e12
+    return {"gathered_bytes_per_launch": gathered, "achieved_tbps": tbps,
+            "ceiling_tbps": ceil["tbps"], "frac": tbps / ceil["tbps"], "source": ceil["source"]}
+
+
 def traffic_for(name, cfg):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -429,7 +448,8 @@ def main():
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "pspmm_spmm_run (zero_split_kernel + spmm_kernel)",
                      "algorithmic_bytes_per_launch": R,
-                     "bytes_formula": "4(n+1) + 8 nnz + 4 n K (B once) + 4 n K (C once)"},
+                     "bytes_formula": "4(n+1) + 8 nnz + 4 n K (B once) + 4 n K (C once)",
+                     "gather": gather_roofline(args.workload, head, K, roof_ms)},
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": sampler.summary(),
