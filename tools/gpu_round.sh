@@ -100,6 +100,14 @@ if want async_ab; then
     ncu -i /tmp/prof_rn_m$m.ncu-rep --page details --csv > $O/ncu_rn_m${m}_details.csv 2>/dev/null
   done
 fi
+if want short_ab; then
+  for v in main s5 s6u2 s5u2 u2 w4 w1 u8; do
+    if [ "$v" = main ]; then unset PSPMM_LIB; else export PSPMM_LIB=$PWD/paper_2605_15695_b200/variants/libpspmm_$v.so; fi
+    timeout 600 python tools/sweep.py --workloads roadnet --VS 10 --modes 3 --Ws 2,4,8 --iters 9 \
+        --out $O/short_$v.json > $O/short_$v.log 2>&1
+  done
+  unset PSPMM_LIB
+fi
 if want diag; then
   for w in reddit products; do
     timeout 600 python tools/e2e_diag.py --workload $w > $O/e2e_diag_$w.json 2> $O/e2e_diag_$w.log
