@@ -6,7 +6,7 @@
 // flight.  Here a row group (G lanes, F float4 accumulators per lane) walks
 // rows r, r + stride, ... with a two-deep software pipeline: the rowPtr pair
 // two rows ahead and the (colIdx, val) of the next row (one vector per lane,
-// rows up to G vectors; longer rows fall back to an inner loop) are in flight
+// rows up to G vectors; longer rows continue in a slow loop) are in flight
 // while the current row's B rows are gathered.  The register footprint stays
 // small (no staged tiles), so more warps are resident.
 #include <algorithm>
@@ -39,16 +39,152 @@ __device__ __forceinline__ float lda(const float *p) {
   return v;
 }
 
-template <int F, int G>
 #ifndef PSPMM_SHORT_MINB
 #define PSPMM_SHORT_MINB 4  // resident 256-thread blocks per SM (register budget)
 #endif
+#ifndef PSPMM_SHORT_WAVES
+#define PSPMM_SHORT_WAVES 1  // grid = one wave of resident blocks (A/B: 1 beats 2 and 4)
+#endif
+#ifndef PSPMM_SHORT_LEAN
+#define PSPMM_SHORT_LEAN 1
+#endif
+
+// FMA of one gathered float4 into an accumulator
+__device__ __forceinline__ void fma4(float4 &acc, float v, const float4 &b) {
+  acc.x = fmaf(v, b.x, acc.x);
+  acc.y = fmaf(v, b.y, acc.y);
+  acc.z = fmaf(v, b.z, acc.z);
+  acc.w = fmaf(v, b.w, acc.w);
+}
+
+#if PSPMM_SHORT_LEAN
+// Lean form: 32-bit row / offset arithmetic, a per-lane B base pointer, and
+// a fast path for the common row (at most U = min(G, 8 / F) vectors: one
+// batch of predicated 128-bit gathers, predicated FMAs, no zero-filled
+// registers); longer rows continue in a generic window loop.
+template <int F, int G>
+__global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const ShortArgs a) {
+  constexpr int U = (8 / F) < G ? (8 / F) : G;  // vectors gathered together
+  const int lane = threadIdx.x & 31;
+  const int g = lane / G, l = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
+  const int groups = (int)((gridDim.x * blockDim.x) >> 5) * (32 / G);
+  int r = a.row_begin + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G) + g;
+  const int col0 = blockIdx.y * G * F * 4;
+  bool cok[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) cok[f] = col0 + (f * G + l) * 4 < a.K;
+  const float4 *bl = reinterpret_cast<const float4 *>(a.B + col0 + l * 4);
+  const uint32_t ldq = (uint32_t)(a.ldb / 4);  // B row stride in float4
+  const int32_t *__restrict__ rowptr = a.rowptr;
+  const int32_t *__restrict__ colidx = a.colidx;
+  const float *__restrict__ val = a.val;
+  const int row_end = a.row_end;
+
+  // pipeline registers: rowPtr of r and r + groups, the vectors of r
+  int h0 = 0, t0 = 0, h1 = 0, t1 = 0;
+  if (r < row_end) {
+    h0 = rowptr[r];
+    t0 = rowptr[r + 1];
+  }
+  if (r + groups < row_end) {
+    h1 = rowptr[r + groups];
+    t1 = rowptr[r + groups + 1];
+  }
+  int c0 = 0;
+  float v0 = 0.f;
+  if (h0 + l < t0) {
+    c0 = lda(colidx + h0 + l);
+    v0 = lda(val + h0 + l);
+  }
+  for (; r < row_end; r += groups) {
+    // prefetch: rowPtr two rows ahead, vectors of the next row
+    const int r2 = r + 2 * groups;
+    int h2 = 0, t2 = 0;
+    if (r2 < row_end) {
+      h2 = rowptr[r2];
+      t2 = rowptr[r2 + 1];
+    }
+    int c1 = 0;
+    float v1 = 0.f;
+    if (h1 + l < t1) {
+      c1 = lda(colidx + h1 + l);
+      v1 = lda(val + h1 + l);
+    }
+    const int cnt = t0 - h0;
+    float4 acc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
+    {  // fast path: the first U vectors
+      float4 b[U][F];
+      float vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = __shfl_sync(gmask, c0, u, G);
+        vv[u] = __shfl_sync(gmask, v0, u, G);
+        const float4 *row = bl + c * ldq;
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+          if (u < cnt && cok[f]) b[u][f] = __ldg(row + f * G);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (u < cnt)
+#pragma unroll
+          for (int f = 0; f < F; ++f)
+            if (cok[f]) fma4(acc[f], vv[u], b[u][f]);
+    }
+    // the rest of a long row: vectors U .. G-1 from the staged window, then
+    // windows of G reloaded from colIdx / val
+    for (int j = U; j < cnt; ++j) {
+      int c;
+      float v;
+      if (j < G) {
+        c = __shfl_sync(gmask, c0, j, G);
+        v = __shfl_sync(gmask, v0, j, G);
+      } else {
+        c = lda(colidx + h0 + j);  // uniform address within the group: broadcast
+        v = lda(val + h0 + j);
+      }
+      const float4 *row = bl + c * ldq;
+#pragma unroll
+      for (int f = 0; f < F; ++f)
+        if (cok[f]) fma4(acc[f], v, __ldg(row + f * G));
+    }
+    float4 *crow = reinterpret_cast<float4 *>(a.C + (int64_t)r * a.ldc + col0 + l * 4);
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+      if (cok[f]) {
+        float4 v = acc[f];
+        if (a.accumulate) {
+          const float4 o = crow[f * G];
+          v.x += o.x;
+          v.y += o.y;
+          v.z += o.z;
+          v.w += o.w;
+        }
+        __stcs(crow + f * G, v);
+#pragma unroll 1
+        for (int d = 0; d < a.fan.n; ++d)
+          __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + (int64_t)r * a.ldc + col0 + l * 4) +
+                     f * G,
+                 v);
+      }
+    h0 = h1;
+    t0 = t1;
+    h1 = h2;
+    t1 = t2;
+    c0 = c1;
+    v0 = v1;
+  }
+  if (a.fan.n) __threadfence_system();
+}
+
+#else
 #ifndef PSPMM_SHORT_UNR
 #define PSPMM_SHORT_UNR 4
 #endif
-#ifndef PSPMM_SHORT_WAVES
-#define PSPMM_SHORT_WAVES 2
-#endif
+template <int F, int G>
 __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const ShortArgs a) {
   constexpr int UNR = PSPMM_SHORT_UNR;  // vectors of a row whose B rows are in flight together
   const int lane = threadIdx.x & 31;
@@ -159,6 +295,8 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
   }
   if (a.fan.n) __threadfence_system();
 }
+
+#endif
 
 using ShortFn = void (*)(const ShortArgs);
 

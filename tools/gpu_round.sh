@@ -101,7 +101,7 @@ if want async_ab; then
   done
 fi
 if want short_ab; then
-  for v in main s5 s6u2 s5u2 u2 w4 w1 u8; do
+  for v in ${SHORT_VARIANTS:-main}; do
     if [ "$v" = main ]; then unset PSPMM_LIB; else export PSPMM_LIB=$PWD/paper_2605_15695_b200/variants/libpspmm_$v.so; fi
     timeout 600 python tools/sweep.py --workloads roadnet --VS 10 --modes 3 --Ws 2,4,8 --iters 9 \
         --out $O/short_$v.json > $O/short_$v.log 2>&1
