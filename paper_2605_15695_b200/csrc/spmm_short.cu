@@ -40,13 +40,15 @@ __device__ __forceinline__ float lda(const float *p) {
 }
 
 #ifndef PSPMM_SHORT_MINB
-#define PSPMM_SHORT_MINB 4  // resident 256-thread blocks per SM (register budget)
+// resident 256-thread blocks per SM: 3 = 85 registers, no spills (A/B on
+// roadNet: 0.148 ms vs 0.156 at 4 blocks / 64 registers with spills)
+#define PSPMM_SHORT_MINB 3
+#endif
+#ifndef PSPMM_SHORT_WIN2
+#define PSPMM_SHORT_WIN2 0  // 1: stage 2G vectors per row (two gather batches)
 #endif
 #ifndef PSPMM_SHORT_WAVES
 #define PSPMM_SHORT_WAVES 1  // grid = one wave of resident blocks (A/B: 1 beats 2 and 4)
-#endif
-#ifndef PSPMM_SHORT_LEAN
-#define PSPMM_SHORT_LEAN 1
 #endif
 
 // FMA of one gathered float4 into an accumulator
@@ -57,7 +59,6 @@ __device__ __forceinline__ void fma4(float4 &acc, float v, const float4 &b) {
   acc.w = fmaf(v, b.w, acc.w);
 }
 
-#if PSPMM_SHORT_LEAN
 // Lean form: 32-bit row / offset arithmetic, a per-lane B base pointer, and
 // a fast path for the common row (at most U = min(G, 8 / F) vectors: one
 // batch of predicated 128-bit gathers, predicated FMAs, no zero-filled
@@ -97,6 +98,14 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
     c0 = lda(colidx + h0 + l);
     v0 = lda(val + h0 + l);
   }
+#if PSPMM_SHORT_WIN2
+  int c0b = 0;  // second staged window: vectors G .. 2G-1
+  float v0b = 0.f;
+  if (h0 + G + l < t0) {
+    c0b = lda(colidx + h0 + G + l);
+    v0b = lda(val + h0 + G + l);
+  }
+#endif
   for (; r < row_end; r += groups) {
     // prefetch: rowPtr two rows ahead, vectors of the next row
     const int r2 = r + 2 * groups;
@@ -111,6 +120,14 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
       c1 = lda(colidx + h1 + l);
       v1 = lda(val + h1 + l);
     }
+#if PSPMM_SHORT_WIN2
+    int c1b = 0;
+    float v1b = 0.f;
+    if (h1 + G + l < t1) {
+      c1b = lda(colidx + h1 + G + l);
+      v1b = lda(val + h1 + G + l);
+    }
+#endif
     const int cnt = t0 - h0;
     float4 acc[F];
 #pragma unroll
@@ -122,7 +139,7 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
       for (int u = 0; u < U; ++u) {
         const int c = __shfl_sync(gmask, c0, u, G);
         vv[u] = __shfl_sync(gmask, v0, u, G);
-        const float4 *row = bl + c * ldq;
+        const float4 *row = bl + (uint64_t)(uint32_t)c * ldq;
 #pragma unroll
         for (int f = 0; f < F; ++f)
           if (u < cnt && cok[f]) b[u][f] = __ldg(row + f * G);
@@ -134,9 +151,34 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
           for (int f = 0; f < F; ++f)
             if (cok[f]) fma4(acc[f], vv[u], b[u][f]);
     }
-    // the rest of a long row: vectors U .. G-1 from the staged window, then
-    // windows of G reloaded from colIdx / val
-    for (int j = U; j < cnt; ++j) {
+#if PSPMM_SHORT_WIN2
+    if (cnt > U) {  // second batch: vectors U .. 2U-1, all staged
+      float4 b[U][F];
+      float vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = U + u;
+        const int c = j < G ? __shfl_sync(gmask, c0, j, G) : __shfl_sync(gmask, c0b, j - G, G);
+        vv[u] = j < G ? __shfl_sync(gmask, v0, j, G) : __shfl_sync(gmask, v0b, j - G, G);
+        const float4 *row = bl + (uint64_t)(uint32_t)c * ldq;
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+          if (j < cnt && cok[f]) b[u][f] = __ldg(row + f * G);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (U + u < cnt)
+#pragma unroll
+          for (int f = 0; f < F; ++f)
+            if (cok[f]) fma4(acc[f], vv[u], b[u][f]);
+    }
+    constexpr int J0 = 2 * U;
+#else
+    constexpr int J0 = U;
+#endif
+    // the rest of a long row: staged vectors J0 .. G-1, then reloads from
+    // colIdx / val
+    for (int j = J0; j < cnt; ++j) {
       int c;
       float v;
       if (j < G) {
@@ -146,7 +188,7 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
         c = lda(colidx + h0 + j);  // uniform address within the group: broadcast
         v = lda(val + h0 + j);
       }
-      const float4 *row = bl + c * ldq;
+      const float4 *row = bl + (uint64_t)(uint32_t)c * ldq;
 #pragma unroll
       for (int f = 0; f < F; ++f)
         if (cok[f]) fma4(acc[f], v, __ldg(row + f * G));
@@ -176,127 +218,13 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
     t1 = t2;
     c0 = c1;
     v0 = v1;
+#if PSPMM_SHORT_WIN2
+    c0b = c1b;
+    v0b = v1b;
+#endif
   }
   if (a.fan.n) __threadfence_system();
 }
-
-#else
-#ifndef PSPMM_SHORT_UNR
-#define PSPMM_SHORT_UNR 4
-#endif
-template <int F, int G>
-__global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const ShortArgs a) {
-  constexpr int UNR = PSPMM_SHORT_UNR;  // vectors of a row whose B rows are in flight together
-  const int lane = threadIdx.x & 31;
-  const int g = lane / G, l = lane % G;
-  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
-  const int64_t groups = ((int64_t)gridDim.x * blockDim.x >> 5) * (32 / G);
-  const int64_t first = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G) + g;
-  const int col0 = blockIdx.y * G * F * 4;
-  bool cok[F];
-#pragma unroll
-  for (int f = 0; f < F; ++f) cok[f] = col0 + (f * G + l) * 4 < a.K;
-  const char *bptr = reinterpret_cast<const char *>(a.B + col0 + l * 4);
-  const uint32_t stride = (uint32_t)(a.ldb * 4);
-
-  int64_t r = a.row_begin + first;
-  // pipeline registers: rowPtr of r and r + groups, the vectors of r
-  int h0 = 0, t0 = 0, h1 = 0, t1 = 0;
-  if (r < a.row_end) {
-    h0 = a.rowptr[r];
-    t0 = a.rowptr[r + 1];
-  }
-  if (r + groups < a.row_end) {
-    h1 = a.rowptr[r + groups];
-    t1 = a.rowptr[r + groups + 1];
-  }
-  int c0 = 0;
-  float v0 = 0.f;
-  if (h0 + l < t0) {
-    c0 = lda(a.colidx + h0 + l);
-    v0 = lda(a.val + h0 + l);
-  }
-  for (; r < a.row_end; r += groups) {
-    // prefetch: rowPtr two rows ahead, vectors of the next row
-    const int64_t r2 = r + 2 * groups;
-    int h2 = 0, t2 = 0;
-    if (r2 < a.row_end) {
-      h2 = a.rowptr[r2];
-      t2 = a.rowptr[r2 + 1];
-    }
-    int c1 = 0;
-    float v1 = 0.f;
-    if (h1 + l < t1) {
-      c1 = lda(a.colidx + h1 + l);
-      v1 = lda(a.val + h1 + l);
-    }
-    float4 acc[F];
-#pragma unroll
-    for (int f = 0; f < F; ++f) acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int base = h0; base < t0; base += G) {
-      int cb = c0;
-      float vb = v0;
-      if (base != h0) {  // rows longer than G vectors: reload this window
-        cb = base + l < t0 ? lda(a.colidx + base + l) : 0;
-        vb = base + l < t0 ? lda(a.val + base + l) : 0.f;
-      }
-      const int cnt = min(G, t0 - base);
-      for (int j0 = 0; j0 < cnt; j0 += UNR) {
-        float4 b[UNR][F];
-        float vv[UNR];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const int j = j0 + u;
-          const int c = __shfl_sync(gmask, cb, j & (G - 1), G);
-          vv[u] = __shfl_sync(gmask, vb, j & (G - 1), G);
-          const char *row = bptr + (uint64_t)(uint32_t)c * stride;
-#pragma unroll
-          for (int f = 0; f < F; ++f) {
-            if (j < cnt && cok[f])
-              b[u][f] = __ldg(reinterpret_cast<const float4 *>(row + f * G * 16));
-            else
-              b[u][f] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u)
-#pragma unroll
-          for (int f = 0; f < F; ++f) {
-            acc[f].x = fmaf(vv[u], b[u][f].x, acc[f].x);
-            acc[f].y = fmaf(vv[u], b[u][f].y, acc[f].y);
-            acc[f].z = fmaf(vv[u], b[u][f].z, acc[f].z);
-            acc[f].w = fmaf(vv[u], b[u][f].w, acc[f].w);
-          }
-      }
-    }
-    float4 *crow = reinterpret_cast<float4 *>(a.C + r * a.ldc + col0 + l * 4);
-#pragma unroll
-    for (int f = 0; f < F; ++f)
-      if (cok[f]) {
-        float4 v = acc[f];
-        if (a.accumulate) {
-          const float4 o = crow[f * G];
-          v.x += o.x;
-          v.y += o.y;
-          v.z += o.z;
-          v.w += o.w;
-        }
-        __stcs(crow + f * G, v);
-#pragma unroll 1
-        for (int d = 0; d < a.fan.n; ++d)
-          __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + r * a.ldc + col0 + l * 4) + f * G, v);
-      }
-    h0 = h1;
-    t0 = t1;
-    h1 = h2;
-    t1 = t2;
-    c0 = c1;
-    v0 = v1;
-  }
-  if (a.fan.n) __threadfence_system();
-}
-
-#endif
 
 using ShortFn = void (*)(const ShortArgs);
 
