@@ -44,9 +44,6 @@ __device__ __forceinline__ float lda(const float *p) {
 // roadNet: 0.148 ms vs 0.156 at 4 blocks / 64 registers with spills)
 #define PSPMM_SHORT_MINB 3
 #endif
-#ifndef PSPMM_SHORT_WIN2
-#define PSPMM_SHORT_WIN2 0  // 1: stage 2G vectors per row (two gather batches)
-#endif
 #ifndef PSPMM_SHORT_WAVES
 #define PSPMM_SHORT_WAVES 1  // grid = one wave of resident blocks (A/B: 1 beats 2 and 4)
 #endif
@@ -98,14 +95,6 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
     c0 = lda(colidx + h0 + l);
     v0 = lda(val + h0 + l);
   }
-#if PSPMM_SHORT_WIN2
-  int c0b = 0;  // second staged window: vectors G .. 2G-1
-  float v0b = 0.f;
-  if (h0 + G + l < t0) {
-    c0b = lda(colidx + h0 + G + l);
-    v0b = lda(val + h0 + G + l);
-  }
-#endif
   for (; r < row_end; r += groups) {
     // prefetch: rowPtr two rows ahead, vectors of the next row
     const int r2 = r + 2 * groups;
@@ -120,14 +109,6 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
       c1 = lda(colidx + h1 + l);
       v1 = lda(val + h1 + l);
     }
-#if PSPMM_SHORT_WIN2
-    int c1b = 0;
-    float v1b = 0.f;
-    if (h1 + G + l < t1) {
-      c1b = lda(colidx + h1 + G + l);
-      v1b = lda(val + h1 + G + l);
-    }
-#endif
     const int cnt = t0 - h0;
     float4 acc[F];
 #pragma unroll
@@ -139,7 +120,7 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
       for (int u = 0; u < U; ++u) {
         const int c = __shfl_sync(gmask, c0, u, G);
         vv[u] = __shfl_sync(gmask, v0, u, G);
-        const float4 *row = bl + (uint64_t)(uint32_t)c * ldq;
+        const float4 *row = bl + (uint32_t)c * ldq;
 #pragma unroll
         for (int f = 0; f < F; ++f)
           if (u < cnt && cok[f]) b[u][f] = __ldg(row + f * G);
@@ -151,34 +132,9 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
           for (int f = 0; f < F; ++f)
             if (cok[f]) fma4(acc[f], vv[u], b[u][f]);
     }
-#if PSPMM_SHORT_WIN2
-    if (cnt > U) {  // second batch: vectors U .. 2U-1, all staged
-      float4 b[U][F];
-      float vv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = U + u;
-        const int c = j < G ? __shfl_sync(gmask, c0, j, G) : __shfl_sync(gmask, c0b, j - G, G);
-        vv[u] = j < G ? __shfl_sync(gmask, v0, j, G) : __shfl_sync(gmask, v0b, j - G, G);
-        const float4 *row = bl + (uint64_t)(uint32_t)c * ldq;
-#pragma unroll
-        for (int f = 0; f < F; ++f)
-          if (j < cnt && cok[f]) b[u][f] = __ldg(row + f * G);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (U + u < cnt)
-#pragma unroll
-          for (int f = 0; f < F; ++f)
-            if (cok[f]) fma4(acc[f], vv[u], b[u][f]);
-    }
-    constexpr int J0 = 2 * U;
-#else
-    constexpr int J0 = U;
-#endif
-    // the rest of a long row: staged vectors J0 .. G-1, then reloads from
-    // colIdx / val
-    for (int j = J0; j < cnt; ++j) {
+    // the rest of a long row: staged vectors U .. G-1, then reloads from
+    // colIdx / val (a second staged window measured slower: more registers)
+    for (int j = U; j < cnt; ++j) {
       int c;
       float v;
       if (j < G) {
@@ -188,7 +144,7 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
         c = lda(colidx + h0 + j);  // uniform address within the group: broadcast
         v = lda(val + h0 + j);
       }
-      const float4 *row = bl + (uint64_t)(uint32_t)c * ldq;
+      const float4 *row = bl + (uint32_t)c * ldq;
 #pragma unroll
       for (int f = 0; f < F; ++f)
         if (cok[f]) fma4(acc[f], v, __ldg(row + f * G));
@@ -218,10 +174,6 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
     t1 = t2;
     c0 = c1;
     v0 = v1;
-#if PSPMM_SHORT_WIN2
-    c0b = c1b;
-    v0b = v1b;
-#endif
   }
   if (a.fan.n) __threadfence_system();
 }
@@ -259,7 +211,9 @@ int ceil_pow2(int x) {
 
 bool short_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc, const float *d_B,
                      const float *d_C, const pspmm_config &cfg) {
+  // B offsets are 32-bit float4 counts: B must span < 2^32 float4 (64 GB)
   return A->V == 1 && A->S == 0 && K % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 &&
+         (uint64_t)A->n_cols * (uint64_t)(ldb / 4) < (1ull << 32) &&
          (reinterpret_cast<uintptr_t>(d_B) & 15) == 0 &&
          (reinterpret_cast<uintptr_t>(d_C) & 15) == 0 &&
          (cfg.F == 1 || cfg.F == 2 || cfg.F == 4);
