@@ -301,6 +301,28 @@ pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,
                                  float *d_t_val, void *stream);
 
 /*
+ * (f3) Dense product of a GNN layer: T = X . W in fp32 (CUDA cores; the
+ * skinny n x Ki by Ki x Ko product is HBM-bound).  X: n x Ki (ldx), W:
+ * Ki x Ko (ldw), T: n x Ko (ldt), all row-major device fp32.  Ki <= 800.
+ * Sequential fp32 accumulation over Ki.  Asynchronous on `stream`.
+ */
+pspmm_status pspmm_dense_gemm(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
+                              const float *d_W, int64_t ldw, float *d_T, int64_t ldt,
+                              void *stream);
+
+/*
+ * (f3) One GCN / GIN-style layer H' = A . H . W (PAPER.md P:21-23,
+ * P:449-460): Y = A . (X . W) when Ko <= Ki, else (A . X) . W, so the SpMM
+ * always runs on min(Ki, Ko) columns; `cfg` is the engine config for that
+ * K (e.g. pspmm_decide_config(features, min(Ki, Ko))).  X: n x Ki, W:
+ * Ki x Ko, Y: n x Ko; T is a caller-owned n x min(Ki, Ko) workspace (ldt).
+ * Errors as pspmm_spmm_run and pspmm_dense_gemm.  Asynchronous.
+ */
+pspmm_status pspmm_gnn_layer(pspmm_pcsr A, const float *d_X, int64_t ldx, int32_t Ki,
+                             const float *d_W, int64_t ldw, int32_t Ko, float *d_T, int64_t ldt,
+                             float *d_Y, int64_t ldy, pspmm_config cfg, void *stream);
+
+/*
  * (f1) Locality reordering (§4.4; Rabbit itself is not
  * reimplemented).  Host function over host CSR arrays; writes
  * perm[old] = new for all n nodes (a bijection).  strategy 0 = identity,

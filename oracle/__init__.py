@@ -10,6 +10,7 @@ Functions (each cites the paper passage it follows, see oracle.c):
   gap(dim, F, omega)                     Eq. 1, P:138-146 (+ c-1a)
   pcsr_build(rowptr, colidx, val, V, S, omega, sg_override=0) -> dict
   features(rowptr, colidx, val, omega)   Table 3, P:307-334 -> dict
+  gnn_layer(rowptr, colidx, val, X, W)  H' = A H W -> (Y, mag)
 """
 from __future__ import annotations
 
@@ -157,3 +158,21 @@ def features(rowptr, colidx, val, omega: int = 32):
     if st:
         raise OracleError(st, "features")
     return dict(zip(FEATURE_NAMES, f.tolist()))
+
+
+def gnn_layer(rowptr, colidx, val, X, W):
+    """f3: one GCN/GIN-style layer H' = A . H . W (where
+    SpMM is the aggregation of a GNN layer; P:449-460 trains GCN and GIN).
+    Plain fp64: T = H . W (numpy matmul), then Y = A . T over the CSR (the
+    definition of P:48 with fp64 values, scipy's CSR product as the library
+    primitive).  mag = |A| . (|H| . |W|) bounds every product term for the
+    c-1 style tolerance.  Test infrastructure only."""
+    import scipy.sparse as sp
+    rowptr, colidx, val = _csr(rowptr, colidx, val)
+    n = rowptr.shape[0] - 1
+    X = np.asarray(X, dtype=np.float64)
+    W = np.asarray(W, dtype=np.float64)
+    A = sp.csr_matrix((val.astype(np.float64), colidx, rowptr), shape=(n, X.shape[0]))
+    Y = A @ (X @ W)
+    mag = abs(A) @ (np.abs(X) @ np.abs(W))
+    return np.asarray(Y), np.asarray(mag)

@@ -108,6 +108,8 @@ _sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
 _sig("pspmm_spmm_accumulate", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host_batch", _st, _P, _P, _i64, _i32, _P, _i64, _i32, Config, _P, _P, _P)
+_sig("pspmm_dense_gemm", _st, _i64, _i32, _i32, _P, _i64, _P, _i64, _P, _i64, _P)
+_sig("pspmm_gnn_layer", _st, _P, _P, _i64, _i32, _P, _i64, _i32, _P, _i64, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_fanout", _st, _P, _P, _i64, _i32, _P, _i64, _P, _i32, Config, _P)
 _sig("pspmm_ipc_get_handle", _st, _P, _P, ctypes.POINTER(_i64))
 _sig("pspmm_ipc_open", _st, _P, ctypes.POINTER(_P))
@@ -327,6 +329,34 @@ def pspmm_spmm_run_host_batch(A: Pcsr, hBs, hCs, cfg: Config, dBs, dCs, stream=N
     DC = (ctypes.c_void_p * 2)(dc[0][0].value, dc[1][0].value)
     _check(_lib.pspmm_spmm_run_host_batch(A.handle, HB, K, K, HC, K, n, cfg, DB, DC,
                                           _stream(stream)), "pspmm_spmm_run_host_batch")
+
+
+def pspmm_dense_gemm(X, W, T, stream=None):
+    """T = X . W (fp32, device)."""
+    x, ldx = _dense(X, "X")
+    w, ldw = _dense(W, "W")
+    t, ldt = _dense(T, "T")
+    n, Ki = X.shape
+    Ko = W.shape[1]
+    if W.shape[0] != Ki or T.shape[0] < n or T.shape[1] < Ko:
+        raise ValueError("X (n x Ki), W (Ki x Ko), T (n x Ko) shapes do not match")
+    _check(_lib.pspmm_dense_gemm(n, Ki, Ko, x, ldx, w, ldw, t, ldt, _stream(stream)),
+           "pspmm_dense_gemm")
+
+
+def pspmm_gnn_layer(A: Pcsr, X, W, T, Y, cfg: Config, stream=None):
+    """Y = A . X . W (the SpMM on min(Ki, Ko) columns; T: n x min(Ki, Ko))."""
+    x, ldx = _dense(X, "X")
+    w, ldw = _dense(W, "W")
+    t, ldt = _dense(T, "T")
+    y, ldy = _dense(Y, "Y")
+    Ki, Ko = W.shape
+    if X.shape[1] != Ki or X.shape[0] < A.n_cols or Y.shape[0] < A.n_rows or Y.shape[1] < Ko:
+        raise ValueError("X (n x Ki), W (Ki x Ko), Y (n x Ko) shapes do not match A")
+    if T.shape[1] < min(Ki, Ko) or T.shape[0] < max(A.n_rows, A.n_cols):
+        raise ValueError("T must be n x min(Ki, Ko)")
+    _check(_lib.pspmm_gnn_layer(A.handle, x, ldx, Ki, w, ldw, Ko, t, ldt, y, ldy, cfg,
+                                _stream(stream)), "pspmm_gnn_layer")
 
 
 MAX_PEERS = 7  # PSPMM_MAX_PEERS

@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -273,6 +274,36 @@ pspmm_status pspmm_spmm_run_host_batch(pspmm_pcsr A, const float *const *h_B, in
     return PSPMM_ERR_DIM_MISMATCH;
   }
   return run_spmm_host_batch(A, h_B, ldb, K, h_C, ldc, count, cfg, d_B, d_C, as_stream(stream));
+}
+
+pspmm_status pspmm_dense_gemm(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
+                              const float *d_W, int64_t ldw, float *d_T, int64_t ldt,
+                              void *stream) {
+  return dense_gemm(n, Ki, Ko, d_X, ldx, d_W, ldw, d_T, ldt, as_stream(stream));
+}
+
+pspmm_status pspmm_gnn_layer(pspmm_pcsr A, const float *d_X, int64_t ldx, int32_t Ki,
+                             const float *d_W, int64_t ldw, int32_t Ko, float *d_T, int64_t ldt,
+                             float *d_Y, int64_t ldy, pspmm_config cfg, void *stream) {
+  if (!A || !d_X || !d_W || !d_T || !d_Y) {
+    set_error("gnn_layer: null argument");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  if (Ki < 1 || Ko < 1 || ldx < Ki || ldw < Ko || ldy < Ko || ldt < std::min(Ki, Ko)) {
+    set_error("gnn_layer: need Ki, Ko >= 1, ldx >= Ki, ldw >= Ko, ldy >= Ko, ldt >= min(Ki, Ko)");
+    return PSPMM_ERR_DIM_MISMATCH;
+  }
+  cudaStream_t s = as_stream(stream);
+  pspmm_status st;
+  if (Ko <= Ki) {  // T = X . W (n_cols x Ko), Y = A . T: the SpMM runs on Ko columns
+    st = dense_gemm(A->n_cols, Ki, Ko, d_X, ldx, d_W, ldw, d_T, ldt, s);
+    if (st != PSPMM_OK) return st;
+    return run_spmm(A, d_T, ldt, Ko, d_Y, ldy, cfg, s);
+  }
+  // T = A . X (n x Ki), Y = T . W: the SpMM runs on Ki columns
+  st = run_spmm(A, d_X, ldx, Ki, d_T, ldt, cfg, s);
+  if (st != PSPMM_OK) return st;
+  return dense_gemm(A->n_rows, Ki, Ko, d_T, ldt, d_W, ldw, d_Y, ldy, s);
 }
 
 pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,

@@ -125,6 +125,11 @@ pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64
                                  const pspmm_config &cfg, float *const *d_B, float *const *d_C,
                                  cudaStream_t stream);
 
+// gnn_layer.cu (f3: the dense product of a GNN layer)
+pspmm_status dense_gemm(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
+                        const float *d_W, int64_t ldw, float *d_T, int64_t ldt,
+                        cudaStream_t stream);
+
 // transpose.cu (f3: backward SpMM operand)
 pspmm_status csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t *d_rowptr,
                            const int32_t *d_colidx, const float *d_val, int32_t *d_t_rowptr,

@@ -1,0 +1,60 @@
+"""(f3) pspmm_dense_gemm and pspmm_gnn_layer (H' = A H W) against the fp64
+oracle (oracle.gnn_layer): both orders (SpMM on the narrower side), ragged
+widths, several engine configs, and the decided config."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from gpu_util import RTOL_MAG, ATOL, dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(Y, ref, mag, what):
+    # c-1 style bound; the fp32 dense product adds at most Ki 2^-24 of the
+    # same magnitude, far inside 1e-5
+    err = np.abs(np.asarray(Y, np.float64) - ref)
+    bad = err > RTOL_MAG * mag + ATOL
+    assert not bad.any(), f"{what}: {int(bad.sum())} elements out of tolerance"
+
+
+@pytest.mark.parametrize("n,Ki,Ko", [(1, 4, 4), (777, 64, 64), (1000, 16, 200), (513, 130, 7),
+                                     (4097, 256, 64)])
+def test_dense_gemm(n, Ki, Ko):
+    import torch
+    from paper_2605_15695_b200 import api
+    X = gen.dense(n, Ki, 11)
+    W = gen.dense(Ki, Ko, 12)
+    T = torch.full((n, Ko), float("nan"), device="cuda")
+    api.pspmm_dense_gemm(torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda(), T)
+    torch.cuda.synchronize()
+    ref = X.astype(np.float64) @ W.astype(np.float64)
+    mag = np.abs(X.astype(np.float64)) @ np.abs(W.astype(np.float64))
+    _check(T.cpu().numpy(), ref, mag, f"gemm {n}x{Ki}x{Ko}")
+
+
+@pytest.mark.parametrize("name", ["reddit_s", "roadnet_s", "empty_rows"])
+@pytest.mark.parametrize("Ki,Ko", [(64, 32), (32, 64), (48, 48), (128, 16)])
+def test_gnn_layer(name, Ki, Ko):
+    import torch
+    from paper_2605_15695_b200 import api
+    g = {"reddit_s": lambda: gen.config_graph("reddit", 0.005),
+         "roadnet_s": lambda: gen.config_graph("roadnet", 0.005),
+         "empty_rows": lambda: gen.with_empty_rows(gen.powerlaw(2000, 12, 2.1, 3), 0.2, 4)}[name]()
+    X = gen.dense(g.n, Ki, 21)
+    W = gen.dense(Ki, Ko, 22)
+    ref, mag = oracle.gnn_layer(g.rowptr, g.colidx, g.val, X, W)
+    rp, ci, vl = dev(g)
+    K = min(Ki, Ko)
+    feats = api.pspmm_features_compute(g.n, g.nnz, rp, ci)
+    cfgs = [api.pspmm_decide_config(feats, K), api.Config(V=1, S=1, W=4),
+            api.Config(V=2, S=0, W=2, F=2)]
+    Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+    for cfg in cfgs:
+        A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, cfg.V, cfg.S)
+        T = torch.empty((g.n, K), device="cuda")
+        Y = torch.full((g.n, Ko), float("nan"), device="cuda")
+        api.pspmm_gnn_layer(A, Xd, Wd, T, Y, cfg)
+        torch.cuda.synchronize()
+        _check(Y.cpu().numpy(), ref, mag, f"layer {name} {Ki}->{Ko} {cfg}")
