@@ -344,6 +344,21 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
                               "zero_split+spmm, D2H -> h_C; 2 rotating device buffer sets, "
                               "copies of neighbouring steps overlap the engine",
                       "single_call_ms": float(np.mean(te))}
+    if want_e2e:
+        # f3: one GNN layer H' = A H W with a K x K weight (SpMM + the dense
+        # product), and the dense product alone
+        Wd = torch.from_numpy(gen.dense(K, K, 4242)).cuda()
+        T = torch.empty((g.n, K), device="cuda")
+        Y = torch.empty((g.n, K), device="cuda")
+        tl = time_steps(lambda: api.pspmm_gnn_layer(A, Bd, Wd, T, Y, cfg, stream), 5, 2, flush,
+                        stream)
+        tg = time_steps(lambda: api.pspmm_dense_gemm(Bd, Wd, T, stream), 5, 2, flush, stream)
+        ml, mg = float(np.mean(tl)), float(np.mean(tg))
+        lf = 2.0 * g.nnz * K + 2.0 * g.n * K * K
+        out["gnn_layer"] = {"ms": ml, "gflops": lf / (ml * 1e-3) / 1e9, "dense_gemm_ms": mg,
+                            "dense_gemm_gbs": 8.0 * g.n * K / (mg * 1e-3) / 1e9,
+                            "what": f"pspmm_gnn_layer: Y = A (X W), W {K}x{K}; flops 2 nnz K + "
+                                    "2 n K^2; dense_gemm_gbs = X read + T written"}
     del A, rp, ci, vl, Bd, C
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -456,7 +471,7 @@ def main():
     }
     if world == 1 and isinstance(head, dict):
         for k in ("cusparse", "speedup_vs_cusparse_best", "speedup_vs_cusparse_default",
-                  "pcsr", "features", "preprocess_s", "ms_median", "ms_min"):
+                  "pcsr", "features", "preprocess_s", "ms_median", "ms_min", "gnn_layer"):
             if k in head:
                 line[k] = head[k]
     if rank == 0 and world == 1:
