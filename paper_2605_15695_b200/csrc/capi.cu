@@ -334,9 +334,4 @@ pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_row
   return compute_features(n, nnz, d_rowptr, d_colidx, omega, as_stream(stream), out);
 }
 
-// experimental A/B knob (not in include/pspmm.h)
-void pspmm_x_set_hot_cols(int64_t h) {
-  pspmm::g_hot_cols = h < 0 || h > 0xffffffffll ? 0xffffffffu : (uint32_t)h;
-}
-
 }  // extern "C"

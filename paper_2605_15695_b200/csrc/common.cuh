@@ -92,7 +92,6 @@ struct Fanout {
 };
 
 // spmm.cu
-extern uint32_t g_hot_cols;  // experimental L2 policy split (spmm.cu)
 pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
                       int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
                       int32_t accumulate = 0, const Fanout *fan = nullptr);

@@ -45,10 +45,6 @@ int ceil_pow2(int64_t x) {
 
 }  // namespace
 
-// Experimental (A/B): B rows below this index are gathered with L2
-// evict_last, the rest evict_first (default: all evict_last).
-uint32_t g_hot_cols = 0xffffffffu;
-
 namespace {
 
 // Validated launch plan of one engine call.
@@ -172,7 +168,6 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
   args.K = K;
   args.accumulate = accumulate;
   args.fan = fan;
-  args.hot_cols = g_hot_cols;
   // the length-sorted unit order applies to whole-matrix launches only (the
   // host entry's slices are contiguous unit ranges)
   args.order = (cfg.order && u0 == 0 && u1 == A->num_chunks) ? A->d_order : nullptr;

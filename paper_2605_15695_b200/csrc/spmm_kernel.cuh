@@ -43,7 +43,6 @@ struct SpmmArgs {
   int32_t n_rows, unit_begin, units, units_total, K;  // units = end of this launch's range
   int32_t accumulate;                                  // 1: C += A.B
   const int32_t *__restrict__ order;                   // optional unit order (nullptr = identity)
-  uint32_t hot_cols;                                   // B rows < hot_cols: L2 evict_last, others evict_first
   Fanout fan;                                          // peer copies of C (f2); fan.n = 0: none
 };
 
@@ -165,8 +164,7 @@ __device__ __forceinline__ void load_tile(const SpmmArgs &a, int base, int tail,
 template <int V, int F, int G, int M, int U, bool VEC, bool FULL, typename T>
 __device__ __forceinline__ void mac_batch(const char *__restrict__ bptr, uint32_t stride,
                                           const bool (&cok)[F], unsigned gmask, int cnt,
-                                          uint64_t pol, uint64_t polf, uint32_t hot,
-                                          const int (&mc)[M],
+                                          uint64_t pol, const int (&mc)[M],
                                           const float (&mv)[M][V], T (&acc)[V][F], int j0) {
   constexpr int FSTEP = G * (VEC ? 16 : 4);  // bytes between a lane's f-th columns
   T b[U][F];
@@ -179,11 +177,10 @@ __device__ __forceinline__ void mac_batch(const char *__restrict__ bptr, uint32_
 #pragma unroll
     for (int k = 0; k < V; ++k) vv[u][k] = __shfl_sync(gmask, mv[m][k], j % G, G);
     const char *row = bptr + (uint64_t)(uint32_t)c * stride;
-    const uint64_t pu = (uint32_t)c < hot ? pol : polf;
 #pragma unroll
     for (int f = 0; f < F; ++f) {
       if ((FULL || j < cnt) && cok[f])
-        ld_b(b[u][f], row + f * FSTEP, pu);
+        ld_b(b[u][f], row + f * FSTEP, pol);
       else
         b[u][f] = zero_v<T>();
     }
@@ -210,21 +207,20 @@ __device__ __forceinline__ void mac_batch(const char *__restrict__ bptr, uint32_
 template <int V, int F, int G, int M, int U, bool VEC, bool FULL, typename T>
 __device__ __forceinline__ void mac_tile(const char *__restrict__ bptr, uint32_t stride,
                                          const bool (&cok)[F], unsigned gmask, int cnt,
-                                         uint64_t pol, uint64_t polf, uint32_t hot,
-                                         const int (&mc)[M],
+                                         uint64_t pol, const int (&mc)[M],
                                          const float (&mv)[M][V], T (&acc)[V][F]) {
   constexpr int TILE = G * M;
   if constexpr (PSPMM_NOHOIST && M == 1 && TILE > U) {
 #pragma unroll 1
     for (int j0 = 0; j0 < TILE; j0 += U) {
       if (FULL || j0 < cnt)
-        mac_batch<V, F, G, M, U, VEC, FULL>(bptr, stride, cok, gmask, cnt, pol, polf, hot, mc, mv, acc, j0);
+        mac_batch<V, F, G, M, U, VEC, FULL>(bptr, stride, cok, gmask, cnt, pol, mc, mv, acc, j0);
     }
   } else {
 #pragma unroll
     for (int j0 = 0; j0 < TILE; j0 += U) {
       if (FULL || j0 < cnt)  // uniform inside the group
-        mac_batch<V, F, G, M, U, VEC, FULL>(bptr, stride, cok, gmask, cnt, pol, polf, hot, mc, mv, acc, j0);
+        mac_batch<V, F, G, M, U, VEC, FULL>(bptr, stride, cok, gmask, cnt, pol, mc, mv, acc, j0);
     }
   }
 }
@@ -309,9 +305,9 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
     if (more) load_tile<V, M, G>(a, base + TILE, tail, l, pol_a, nc, nv);
     const int cnt = tail - base;
     if (cnt >= TILE)
-      mac_tile<V, F, G, M, U, VEC, true>(bptr, stride, cok, gmask, cnt, pol_b, pol_a, a.hot_cols, mc, mv, acc);
+      mac_tile<V, F, G, M, U, VEC, true>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
     else
-      mac_tile<V, F, G, M, U, VEC, false>(bptr, stride, cok, gmask, cnt, pol_b, pol_a, a.hot_cols, mc, mv, acc);
+      mac_tile<V, F, G, M, U, VEC, false>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
     if (more) {
 #pragma unroll
       for (int m = 0; m < M; ++m) {
