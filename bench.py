@@ -112,7 +112,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 # workloads
 # ----------------------------------------------------------------------------
-WORKLOADS = ["cora", "roadnet", "products", "proteins", "reddit"]
+WORKLOADS = ["cora", "roadnet", "products", "proteins", "reddit", "proteins_clustered"]
 
 
 def load_graph(name):
@@ -286,17 +286,29 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
                              stream)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
+    # engine mode 1 (dense 128 x 32 tiles on tcgen05 + the rest): split once
+    # per graph, taken when the tiles hold enough of A
+    cfg, dense = api.auto_dense(A, rp, ci, vl, K, cfg, stream)
+    if dense is not None:
+        dense["dense_frac"] = dense["nnz_dense"] / max(1, g.nnz)
+    t3 = time.perf_counter()
     B = gen.config_B(g.name, g.n)
     Bd = torch.from_numpy(B).cuda()
     C = torch.empty((g.n, K), device="cuda")
     launches_per_step = 1 + (1 if (A.info["S"] == 1 and A.info["num_chunks"] > A.info["num_panels"])
-                             else 0)
+                             else 0) + (2 if cfg.mode == 1 else 0)  # mode 1: + split_b + dense_tc
 
     def step():
         A.run(Bd, C, cfg, stream)
 
     ts = time_steps(step, steps, warmup, flush, stream, sampler)
     ms = float(np.mean(ts))
+    mode0 = None
+    if cfg.mode == 1:  # the same knobs on the mode-0 engine alone, for comparison
+        c0 = api.Config(**cfg.as_dict())
+        c0.mode = 0
+        t0s = time_steps(lambda: A.run(Bd, C, c0, stream), steps, warmup, flush, stream)
+        mode0 = {"cfg": c0.as_dict(), "ms_median": float(np.median(t0s))}
     R = algorithmic_bytes(g.n, g.n, g.nnz, K)
     flops = 2.0 * g.nnz * K
     out = {
@@ -306,8 +318,13 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
         "ms_mean": ms, "ms_median": float(np.median(ts)), "ms_min": float(min(ts)),
         "gflops": flops / (ms * 1e-3) / 1e9, "algorithmic_bytes": R,
         "achieved_gbs": R / (ms * 1e-3) / 1e9, "launches_per_step": launches_per_step,
-        "preprocess_s": {"features_decide": t1 - t0, "pcsr_build": t2 - t1},
+        "preprocess_s": {"features_decide": t1 - t0, "pcsr_build": t2 - t1,
+                         "dense_split": t3 - t2},
     }
+    if dense is not None:
+        out["dense_split"] = dense
+    if mode0 is not None:
+        out["mode0_same_knobs"] = mode0
     if want_cusparse:
         cs = cusparse_best(g, rp, ci, vl, Bd, K, steps, flush, stream)
         out["cusparse"] = cs

@@ -269,9 +269,8 @@ def banded(n, half_width, seed, fill=0.7, kind="uniform"):
     return _finish(f"banded_n{n}_h{half_width}", n, rowptr, colidx, seed + 1000, kind=kind)
 
 
-def community(n, csize, d, p_in, seed, ordered=True, kind="uniform"):
-    """Communities of csize nodes; a p_in share of each row's edges stays in
-    its community.  ordered=True keeps community-contiguous IDs."""
+def _community_pattern(n, csize, d, p_in, seed, ordered=True):
+    """(rowptr, colidx) of community(); see there."""
     rng = np.random.default_rng(seed)
     deg = rng.poisson(d, n)
     rows = np.repeat(np.arange(n, dtype=np.int64), deg)
@@ -283,7 +282,13 @@ def community(n, csize, d, p_in, seed, ordered=True, kind="uniform"):
     if not ordered:
         perm = rng.permutation(n).astype(np.int64)
         rows, cols = perm[rows], perm[cols]
-    rowptr, colidx = csr_from_pairs(n, rows, cols)
+    return csr_from_pairs(n, rows, cols)
+
+
+def community(n, csize, d, p_in, seed, ordered=True, kind="uniform"):
+    """Communities of csize nodes; a p_in share of each row's edges stays in
+    its community.  ordered=True keeps community-contiguous IDs."""
+    rowptr, colidx = _community_pattern(n, csize, d, p_in, seed, ordered)
     return _finish(f"community_n{n}_c{csize}", n, rowptr, colidx, seed + 1000, kind=kind)
 
 
@@ -329,6 +334,12 @@ CONFIGS = {
                      d_max=7750),
     "reddit":   dict(n=232965, nnz=114615892, K=64, seeds=(5, 1005, 2005, 3005),
                      d_max=21657),
+    # SURVEY §8(d) proteins variant (ii), for the dense-panel path (a6):
+    # communities of 1024 community-ordered nodes, half of each row's
+    # Poisson(597) draws inside its community (~25 % dense diagonal blocks
+    # after duplicates are dropped, ~74M nnz realized), half uniform
+    "proteins_clustered": dict(n=132534, nnz=79122504, K=256, seeds=(6, 1006, 2006, None),
+                               csize=1024, p_in=0.5),
 }
 
 
@@ -341,7 +352,7 @@ def config_graph(name: str, scale: float = 1.0) -> Graph:
     # (so small graphs stay sparse), d_max scaled like the mean
     n = max(64, int(round(c["n"] * scale)))
     d = c["nnz"] / c["n"]
-    cap = n / 32.0 if name == "proteins" else n / 8.0  # proteins: 8 dense blocks
+    cap = n / 32.0 if name.startswith("proteins") else n / 8.0  # proteins: 8 dense blocks
     shrink = 1.0 if scale >= 1.0 else min(1.0, cap / d)
     nnz = int(round(n * d * shrink)) if scale < 1.0 else c["nnz"]
     nnz -= nnz % 2
@@ -351,6 +362,9 @@ def config_graph(name: str, scale: float = 1.0) -> Graph:
         rowptr, colidx = chung_lu(n, nnz, d_max, gs, shuffle_seed=ss)
     elif name == "roadnet":
         rowptr, colidx = roadnet_like(n, nnz, gs)
+    elif name == "proteins_clustered":
+        dd = d * shrink if scale < 1.0 else d
+        rowptr, colidx = _community_pattern(n, c["csize"], dd, c["p_in"], gs)
     elif name == "proteins":
         blocks = 8
         d_max = max(8, min(n // blocks - 1, int(round(c["d_max"] * shrink))))

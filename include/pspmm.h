@@ -76,8 +76,13 @@ typedef enum {
  *     4 = short-row stream with cp.async shared-memory rings: a row group
  *     owns a contiguous row range and streams its vectors, B rows of 3
  *     batches ahead in flight (same constraints as 3; W, F, G apply);
- *     1 is reserved for a dense-panel tensor-core path and returns
- *     PSPMM_ERR_UNSUPPORTED.
+ *     1 = dense-panel tensor-core path: the dense 128 x 32 tiles attached by
+ *     pspmm_pcsr_attach_dense run on tcgen05 (kind::tf32, 3xTF32 split,
+ *     fp32 accumulators in TMEM), the remaining nonzeros on the mode-0
+ *     engine (W, F, G, order apply to it); needs an attached split (else
+ *     PSPMM_ERR_UNSUPPORTED), K % 16 == 0, ld % 4 == 0, 16-B aligned B and
+ *     C; not with the fan-out entry (the host entries run it whole,
+ *     without slices).
  *  order  mode 0 only: 1 = visit units by descending vector count (a
  *     schedule built with the PCSR; helps skewed, shuffled graphs, hurts
  *     locality-ordered ones), 0 = in storage order.
@@ -220,6 +225,43 @@ pspmm_status pspmm_spmm_run(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t
  */
 pspmm_status pspmm_spmm_accumulate(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
                                    float *d_C, int64_t ldc, pspmm_config cfg, void *stream);
+
+/*
+ * (a6, conditional: SURVEY §8 a6 "dense-panel variant") Split A for engine
+ * mode 1.  The paper's blocking groups rows into panels so a
+ * B row serves several rows; where a 128-row panel is dense over a column
+ * range the product is a real dense contraction.  (d_rowptr, d_colidx,
+ * d_val) must be the CSR A was built from (device, caller-owned, read
+ * only; validated, and nnz must match).  Every 128 x 32 tile (rows
+ * [128p, 128p + 128), columns [32t, 32t + 32)) holding at least
+ * ceil(min_density * 4096) nonzeros is stored densely inside the handle;
+ * the other nonzeros get a PCSR of their own (the handle's V, S, omega;
+ * SG from Eq. 3).  The split also holds scratch for the per-run TF32
+ * images of B (2 x 16 bytes x n_cols x k_max, rounded up), so mode-1 runs
+ * allocate nothing; they accept K <= k_max.  Replaces a previous split;
+ * freed by pspmm_pcsr_destroy.  min_density in (0, 1] and k_max a positive
+ * multiple of 16, else INVALID_ARG.  *out_tiles (may be NULL) =
+ * number of dense tiles.  Runs on the host; synchronises `stream`.  The
+ * bit-exact PCSR arrays of A are untouched.
+ */
+pspmm_status pspmm_pcsr_attach_dense(pspmm_pcsr A, const int32_t *d_rowptr,
+                                     const int32_t *d_colidx, const float *d_val,
+                                     double min_density, int32_t k_max, void *stream,
+                                     int64_t *out_tiles);
+
+/*
+ * Mode-1 decision (host, pure given the handle): cfg->mode = 1 iff a split
+ * is attached, it has dense tiles, K % 16 == 0 and the tiles hold at least
+ * min_frac of A's nonzeros; otherwise a mode of 1 is reset to 0 and any
+ * other mode is left alone.  The remaining knobs (W, F, G, order) are the
+ * ones the rest runs with.  min_frac in [0, 1] else INVALID_ARG.
+ */
+pspmm_status pspmm_decide_dense(pspmm_pcsr A, int32_t K, double min_frac, pspmm_config *cfg);
+
+/* Sizes of the attached split (zeros when none): 128-row panels with dense
+ * tiles, dense tiles, nonzeros inside them. */
+pspmm_status pspmm_pcsr_dense_info(pspmm_pcsr A, int64_t *num_panels, int64_t *num_tiles,
+                                   int64_t *nnz_dense);
 
 /*
  * End-to-end variant for host-resident B and C (bench.py "e2e"): copies

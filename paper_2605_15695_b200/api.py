@@ -107,6 +107,11 @@ _sig("pspmm_pcsr_load", _st, ctypes.c_char_p, _P, ctypes.POINTER(_P))
 _sig("pspmm_spmm_run", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_host", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P, _P, _P)
 _sig("pspmm_spmm_accumulate", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
+_sig("pspmm_pcsr_attach_dense", _st, _P, _P, _P, _P, ctypes.c_double, _i32, _P,
+     ctypes.POINTER(_i64))
+_sig("pspmm_decide_dense", _st, _P, _i32, ctypes.c_double, ctypes.POINTER(Config))
+_sig("pspmm_pcsr_dense_info", _st, _P, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+     ctypes.POINTER(_i64))
 _sig("pspmm_spmm_run_host_batch", _st, _P, _P, _i64, _i32, _P, _i64, _i32, Config, _P, _P, _P)
 _sig("pspmm_dense_gemm", _st, _i64, _i32, _i32, _P, _i64, _P, _i64, _P, _i64, _P)
 _sig("pspmm_gnn_layer", _st, _P, _P, _i64, _i32, _P, _i64, _i32, _P, _i64, _P, _i64, Config, _P)
@@ -294,6 +299,36 @@ def pspmm_spmm_accumulate(A: Pcsr, B, C, cfg: Config, stream=None, K=None):
         raise ValueError("B / C shapes do not match the PCSR handle and K")
     _check(_lib.pspmm_spmm_accumulate(A.handle, b, ldb, K, c, ldc, cfg, _stream(stream)),
            "pspmm_spmm_accumulate")
+
+
+def pspmm_pcsr_attach_dense(A: Pcsr, rowptr, colidx, val, min_density, k_max=256,
+                            stream=None) -> dict:
+    """Split A for engine mode 1: dense 128 x 32 tiles (>= min_density full)
+    on the tensor cores, the rest on the mode-0 engine.  (rowptr, colidx,
+    val) = the device CSR A was built from.  Returns pspmm_pcsr_dense_info."""
+    torch = _torch()
+    nt = _i64()
+    st = _lib.pspmm_pcsr_attach_dense(A.handle, _dev(rowptr, torch.int32, "rowptr"),
+                                      _dev(colidx, torch.int32, "colidx"),
+                                      _dev(val, torch.float32, "val"), float(min_density),
+                                      int(k_max), _stream(stream), ctypes.byref(nt))
+    _check(st, "pspmm_pcsr_attach_dense")
+    return pspmm_pcsr_dense_info(A)
+
+
+def pspmm_decide_dense(A: Pcsr, K: int, min_frac: float, cfg: Config) -> Config:
+    """Mode-1 rule of the C library (include/pspmm.h); returns a new Config."""
+    out = Config(**cfg.as_dict())
+    _check(_lib.pspmm_decide_dense(A.handle, K, float(min_frac), ctypes.byref(out)),
+           "pspmm_decide_dense")
+    return out
+
+
+def pspmm_pcsr_dense_info(A: Pcsr) -> dict:
+    p, t, z = _i64(), _i64(), _i64()
+    _check(_lib.pspmm_pcsr_dense_info(A.handle, ctypes.byref(p), ctypes.byref(t), ctypes.byref(z)),
+           "pspmm_pcsr_dense_info")
+    return {"num_panels": p.value, "num_tiles": t.value, "nnz_dense": z.value}
 
 
 def pspmm_spmm_run_host_batch(A: Pcsr, hBs, hCs, cfg: Config, dBs, dCs, stream=None):
@@ -546,6 +581,24 @@ def auto_config(n, nnz, rowptr, colidx, K, stream=None) -> Config:
     """Phase 1 of P:192: Table-3 features on the device, then the decider."""
     f = pspmm_features_compute(n, nnz, rowptr, colidx, stream=stream)
     return pspmm_decide_config(f, K)
+
+
+# engine mode 1 rule (DESIGN.md §5): 128 x 32 tiles with >= 10 % nonzeros go
+# to the tensor cores when they hold >= 5 % of A's nonzeros
+DENSE_MIN_DENSITY = 0.1
+DENSE_MIN_FRAC = 0.05
+
+
+def auto_dense(A: Pcsr, rowptr, colidx, val, K, cfg: Config, stream=None):
+    """Attach the dense-tile split (K % 16 == 0) and apply the library's
+    mode-1 rule; returns (cfg, split info or None)."""
+    if K % 16 != 0:
+        return cfg, None
+    info = pspmm_pcsr_attach_dense(A, rowptr, colidx, val, DENSE_MIN_DENSITY, k_max=K,
+                                   stream=stream)
+    cfg = pspmm_decide_dense(A, K, DENSE_MIN_FRAC, cfg)
+    info.update(min_density=DENSE_MIN_DENSITY, min_frac=DENSE_MIN_FRAC, taken=cfg.mode == 1)
+    return cfg, info
 
 
 def spmm(rowptr, colidx, val, B, cfg: Config | None = None, stream=None, C=None):

@@ -170,6 +170,7 @@ void pspmm_pcsr_destroy(pspmm_pcsr A) {
     for (cudaEvent_t e : {A->h2d_done[b], A->comp_done[b], A->d2h_done[b]})
       if (e) cudaEventDestroy(e);
   if (A->batch_start) cudaEventDestroy(A->batch_start);
+  destroy_dense(A->dense);
   delete A;
 }
 
@@ -332,6 +333,39 @@ pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_row
                                     const int32_t *d_colidx, int32_t omega, void *stream,
                                     pspmm_features *out) {
   return compute_features(n, nnz, d_rowptr, d_colidx, omega, as_stream(stream), out);
+}
+
+pspmm_status pspmm_pcsr_attach_dense(pspmm_pcsr A, const int32_t *d_rowptr,
+                                     const int32_t *d_colidx, const float *d_val,
+                                     double min_density, int32_t k_max, void *stream,
+                                     int64_t *out_tiles) {
+  return attach_dense(A, d_rowptr, d_colidx, d_val, min_density, k_max, as_stream(stream),
+                      out_tiles);
+}
+
+pspmm_status pspmm_decide_dense(pspmm_pcsr A, int32_t K, double min_frac, pspmm_config *cfg) {
+  if (!A || !cfg || K < 1 || !(min_frac >= 0.0 && min_frac <= 1.0)) {
+    set_error("decide_dense: null argument, K < 1 or min_frac outside [0, 1]");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  if (A->dense && A->dense->num_tiles > 0 && K % 16 == 0 && A->nnz > 0 &&
+      (double)A->dense->nnz_dense >= min_frac * (double)A->nnz)
+    cfg->mode = 1;
+  else if (cfg->mode == 1)
+    cfg->mode = 0;
+  return PSPMM_OK;
+}
+
+pspmm_status pspmm_pcsr_dense_info(pspmm_pcsr A, int64_t *num_panels, int64_t *num_tiles,
+                                   int64_t *nnz_dense) {
+  if (!A || !num_panels || !num_tiles || !nnz_dense) {
+    set_error("pcsr_dense_info: null argument");
+    return PSPMM_ERR_INVALID_ARG;
+  }
+  *num_panels = A->dense ? A->dense->num_panels : 0;
+  *num_tiles = A->dense ? A->dense->num_tiles : 0;
+  *nnz_dense = A->dense ? A->dense->nnz_dense : 0;
+  return PSPMM_OK;
 }
 
 }  // extern "C"

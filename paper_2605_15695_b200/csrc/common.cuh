@@ -15,6 +15,20 @@
 //   slice_*  = kSlices + 1 unit / row bounds at panel boundaries, used by the
 //              host entry to overlap the D2H copy of C with the engine.
 constexpr int kSlices = 8;
+struct pspmm_pcsr_s;
+// Engine mode 1 (spmm_dense.cu): the dense 128 x 32 tiles of A and a PCSR of
+// the remaining nonzeros, attached by pspmm_pcsr_attach_dense.
+struct DenseTiles {
+  int64_t num_panels = 0, num_tiles = 0, nnz_dense = 0, kgroups = 0;
+  int32_t k_max = 0;
+  float *d_tiles = nullptr;        // num_tiles x (TF32 hi 4096, lo 4096), smem image order
+  float4 *d_bhi = nullptr;         // kgroups x k_max: per-run TF32 hi / lo images of B
+  float4 *d_blo = nullptr;
+  int32_t *d_panel_ptr = nullptr;  // num_panels + 1
+  int32_t *d_panel = nullptr;      // num_panels: 128-row panel index
+  int32_t *d_tile_col = nullptr;   // num_tiles: first column of the tile
+  pspmm_pcsr_s *rest = nullptr;    // A minus the dense tiles (same V, S, omega)
+};
 struct pspmm_pcsr_s {
   int64_t n_rows = 0, n_cols = 0, num_panels = 0, nnz = 0, nnz_v = 0, num_chunks = 0;
   int64_t sg = 0, rowptr_len = 0, num_split = 0;
@@ -34,6 +48,7 @@ struct pspmm_pcsr_s {
   // pspmm_spmm_run_host_batch: copy-in / copy-out streams and per-buffer events
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {}, batch_start = nullptr;
+  DenseTiles *dense = nullptr;         // engine mode 1 (pspmm_pcsr_attach_dense)
 };
 
 namespace pspmm {
@@ -90,6 +105,17 @@ struct Fanout {
   float *peer[kMaxPeers];
   int32_t n;
 };
+
+// spmm_dense.cu (engine mode 1)
+bool dense_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc, const float *d_B,
+                     const float *d_C);
+pspmm_status run_spmm_dense(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
+                            float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
+                            int32_t accumulate);
+pspmm_status attach_dense(pspmm_pcsr_s *A, const int32_t *d_rowptr, const int32_t *d_colidx,
+                          const float *d_val, double min_density, int32_t k_max,
+                          cudaStream_t stream, int64_t *out_tiles);
+void destroy_dense(DenseTiles *D);
 
 // spmm.cu
 pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,

@@ -63,7 +63,8 @@ pspmm_status make_plan(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int
     PSPMM_FAIL(PSPMM_ERR_CONFIG_MISMATCH, "spmm_run: cfg.V/S/omega differ from the PCSR handle");
   if (cfg.mode != 0 && cfg.mode != 2 && cfg.mode != 3 && cfg.mode != 4)
     PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
-               "spmm_run: mode must be 0 (LDG engine), 2 (TMA gather), 3 (short rows) or 4 "
+               "spmm_run: mode must be 0 (LDG engine), 1 (dense tiles on tensor cores; "
+               "pspmm_spmm_run / accumulate only), 2 (TMA gather), 3 (short rows) or 4 "
                "(async-copy short rows)");
   if (!(cfg.W == 1 || cfg.W == 2 || cfg.W == 4 || cfg.W == 8))
     PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: W must be 1, 2, 4 or 8");
@@ -204,6 +205,12 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
     }
     f = *fan;
   }
+  if (cfg.mode == 1) {  // dense tiles on the tensor cores + the rest (spmm_dense.cu)
+    if (f.n > 0) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run_fanout: no peer copies in mode 1");
+    if (A && (cfg.V != A->V || cfg.S != A->S || cfg.omega != A->omega))
+      PSPMM_FAIL(PSPMM_ERR_CONFIG_MISMATCH, "spmm_run: cfg.V/S/omega differ from the PCSR handle");
+    return run_spmm_dense(A, d_B, ldb, K, d_C, ldc, cfg, stream, accumulate);
+  }
   Plan plan;
   pspmm_status st = make_plan(A, d_B, ldb, K, d_C, ldc, cfg, &plan);
   if (st != PSPMM_OK) return st;
@@ -235,6 +242,16 @@ pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32
                            cudaStream_t stream) {
   if (!A || !h_B || !h_C)
     PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_host: null handle or host pointer");
+  if (cfg.mode == 1) {  // dense tiles + rest: one whole-matrix product, no slices
+    PSPMM_CUDA_TRY(cudaMemcpyAsync(d_Bbuf, h_B, (size_t)A->n_cols * ldb * sizeof(float),
+                                   cudaMemcpyHostToDevice, stream));
+    pspmm_status st = run_spmm(A, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, stream);
+    if (st != PSPMM_OK) return st;
+    PSPMM_CUDA_TRY(cudaMemcpyAsync(h_C, d_Cbuf, (size_t)A->n_rows * ldc * sizeof(float),
+                                   cudaMemcpyDeviceToHost, stream));
+    PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
+    return PSPMM_OK;
+  }
   Plan plan;
   pspmm_status st = make_plan(A, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, &plan);
   if (st != PSPMM_OK) return st;
@@ -285,7 +302,7 @@ pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64
                                  const pspmm_config &cfg, float *const *d_B, float *const *d_C,
                                  cudaStream_t stream) {
   Plan plan[2];
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < 2 && cfg.mode != 1; ++b) {
     pspmm_status st = make_plan(A, d_B[b], ldb, K, d_C[b], ldc, cfg, &plan[b]);
     if (st != PSPMM_OK) return st;
   }
@@ -315,10 +332,15 @@ pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64
     PSPMM_CUDA_TRY(cudaEventRecord(A->h2d_done[b], A->h2d_stream));
     PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->h2d_done[b], 0));
     if (i >= 2) PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->d2h_done[b], 0));
-    pspmm_status st = prepare_c(A, K, d_C[b], ldc, stream, none);
-    if (st != PSPMM_OK) return st;
-    st = launch_range(A, plan[b], d_B[b], ldb, K, d_C[b], ldc, cfg, stream, 0, A->num_chunks, 0,
-                      none);
+    pspmm_status st;
+    if (cfg.mode == 1) {  // dense tiles + rest (validates its own arguments)
+      st = run_spmm(A, d_B[b], ldb, K, d_C[b], ldc, cfg, stream);
+    } else {
+      st = prepare_c(A, K, d_C[b], ldc, stream, none);
+      if (st != PSPMM_OK) return st;
+      st = launch_range(A, plan[b], d_B[b], ldb, K, d_C[b], ldc, cfg, stream, 0, A->num_chunks, 0,
+                        none);
+    }
     if (st != PSPMM_OK) return st;
     PSPMM_CUDA_TRY(cudaEventRecord(A->comp_done[b], stream));
     PSPMM_CUDA_TRY(cudaStreamWaitEvent(A->d2h_stream, A->comp_done[b], 0));

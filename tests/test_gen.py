@@ -24,7 +24,8 @@ def canonical(g):
     lambda: gen.giant_row(300, 290, 3, 1),
     lambda: gen.config_graph("cora"), lambda: gen.config_graph("reddit", 0.002),
     lambda: gen.config_graph("products", 0.0005), lambda: gen.config_graph("proteins", 0.002),
-    lambda: gen.config_graph("roadnet", 0.001)])
+    lambda: gen.config_graph("roadnet", 0.001),
+    lambda: gen.config_graph("proteins_clustered", 0.02)])
 def test_deterministic_and_canonical(make):
     a, b = make(), make()
     canonical(a)
@@ -62,3 +63,20 @@ def test_config_shapes_small():
     rows = np.repeat(np.arange(r.n), deg)
     W = int(np.ceil(np.sqrt(r.n)))
     assert np.abs(rows - r.colidx).max() <= W + 1
+
+
+def test_proteins_clustered_shape():
+    """SURVEY §8(d) variant (ii): about half of each row's draws stay in its
+    1024-node community, so the diagonal 1024-blocks hold ~half the nonzeros
+    (a little less after duplicates), plus the uniform draws that land in
+    the row's own community by chance (1024 / n of them)."""
+    g = gen.config_graph("proteins_clustered", 0.05)
+    rows = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+    inside = (rows // 1024) == (g.colidx // 1024)
+    frac = inside.mean()
+    expect = 0.5 + 0.5 * 1024 / g.n
+    assert expect - 0.06 < frac < expect + 0.01, (frac, expect)
+    # community-ordered IDs: the in-community share per 1024-row block is flat
+    blocks = rows // 1024
+    per = np.bincount(blocks, weights=inside) / np.bincount(blocks)
+    assert per[:-1].min() > 0.35

@@ -21,7 +21,8 @@ def sample_rows(g, count, seed):
     return np.unique(rows).astype(np.int64)
 
 
-@pytest.mark.parametrize("name", ["cora", "roadnet", "reddit", "proteins", "products"])
+@pytest.mark.parametrize("name", ["cora", "roadnet", "reddit", "proteins", "products",
+                                  "proteins_clustered"])
 def test_full_config(name):
     import torch
     from paper_2605_15695_b200 import api
@@ -38,6 +39,9 @@ def test_full_config(name):
     assert np.array_equal(e["val"].view(np.uint32), ref["val"].view(np.uint32))
     assert np.array_equal(e["TRow"], ref["TRow"])
     del e, ref
+    cfg, dense = api.auto_dense(A, rp, ci, vl, K, cfg)  # engine mode 1 rule, as bench.py
+    if name == "proteins_clustered":
+        assert cfg.mode == 1 and dense["nnz_dense"] > 0.3 * g.nnz
     # SpMM, sampled rows (every row for Cora)
     B = gen.config_B(name, g.n)
     Bd = torch.from_numpy(B).cuda()

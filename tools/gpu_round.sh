@@ -27,13 +27,19 @@ fi
 if want ncu; then
   # full captures are summarised here (JSON) and only the headline report is
   # kept: gpurun_out/ must stay under 64 MiB or nothing comes back
-  for w in reddit roadnet products proteins cora; do
+  for w in reddit roadnet products proteins cora proteins_clustered; do
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm -s 1 -c 1 \
         -o /tmp/prof_$w -f python tools/run_kernel.py --workload $w --iters 2 > $O/ncu_$w.log 2>&1
     python tools/ncu_summary.py /tmp/prof_$w.ncu-rep --json $O/ncu_$w.json > /dev/null 2>&1
     ncu -i /tmp/prof_$w.ncu-rep --page details --csv > $O/ncu_${w}_details.csv 2>/dev/null
   done
   cp /tmp/prof_reddit.ncu-rep $O/ 2>/dev/null
+  # engine mode 1: the tcgen05 dense-tile kernel on the clustered proteins graph
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:dense_tc -s 1 -c 1 \
+      -o /tmp/prof_dense -f python tools/run_kernel.py --workload proteins_clustered --iters 2 \
+      --dense 0.1 > $O/ncu_dense.log 2>&1
+  python tools/ncu_summary.py /tmp/prof_dense.ncu-rep --json $O/ncu_dense.json > /dev/null 2>&1
+  ncu -i /tmp/prof_dense.ncu-rep --page details --csv > $O/ncu_dense_details.csv 2>/dev/null
 fi
 if want sweep; then
   timeout 1800 python tools/sweep.py --workloads cora,roadnet,reddit,proteins,products --iters 5 \

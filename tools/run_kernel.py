@@ -19,6 +19,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="reddit")
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--dense", type=float, default=0.0,
+                    help="> 0: attach the dense-tile split (min density) and run mode 1")
     for k in ("V", "S", "F", "G", "W", "sg", "mode", "order"):
         ap.add_argument(f"--{k}", type=int, default=None)
     a = ap.parse_args()
@@ -33,6 +35,9 @@ def main():
     if a.sg is not None:
         cfg.sg_override = a.sg
     A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, cfg.V, cfg.S, cfg.omega, cfg.sg_override)
+    if a.dense > 0:
+        print(api.pspmm_pcsr_attach_dense(A, rp, ci, vl, a.dense, k_max=g.K))
+        cfg.mode = 1
     B = torch.from_numpy(gen.config_B(g.name, g.n)).cuda()
     C = torch.empty((g.n, g.K), device="cuda")
     for _ in range(a.iters):
