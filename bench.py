@@ -296,7 +296,7 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
     Bd = torch.from_numpy(B).cuda()
     C = torch.empty((g.n, K), device="cuda")
     launches_per_step = 1 + (1 if (A.info["S"] == 1 and A.info["num_chunks"] > A.info["num_panels"])
-                             else 0) + (2 if cfg.mode == 1 else 0)  # mode 1: + split_b + dense_tc
+                             else 0) + (2 if cfg.mode == 1 else 0)  # mode 1: + split_b, dense_tc
 
     def step():
         A.run(Bd, C, cfg, stream)
