@@ -253,8 +253,11 @@ pspmm_status pspmm_pcsr_attach_dense(pspmm_pcsr A, const int32_t *d_rowptr,
  * Mode-1 decision (host, pure given the handle): cfg->mode = 1 iff a split
  * is attached, it has dense tiles, K % 16 == 0 and the tiles hold at least
  * min_frac of A's nonzeros; otherwise a mode of 1 is reset to 0 and any
- * other mode is left alone.  The remaining knobs (W, F, G, order) are the
- * ones the rest runs with.  min_frac in [0, 1] else INVALID_ARG.
+ * other mode is left alone.  When it switches to mode 1 it also sets the
+ * knobs the rest runs with (W, F, G, order) to pspmm_decide_config's pick
+ * for the rest's own Table-3 features (computed by pspmm_pcsr_attach_dense;
+ * kept as given when unavailable or when that pick is a mode-2 label).
+ * min_frac in [0, 1] else INVALID_ARG.
  */
 pspmm_status pspmm_decide_dense(pspmm_pcsr A, int32_t K, double min_frac, pspmm_config *cfg);
 

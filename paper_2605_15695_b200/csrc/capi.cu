@@ -349,9 +349,19 @@ pspmm_status pspmm_decide_dense(pspmm_pcsr A, int32_t K, double min_frac, pspmm_
     return PSPMM_ERR_INVALID_ARG;
   }
   if (A->dense && A->dense->num_tiles > 0 && K % 16 == 0 && A->nnz > 0 &&
-      (double)A->dense->nnz_dense >= min_frac * (double)A->nnz)
+      (double)A->dense->nnz_dense >= min_frac * (double)A->nnz) {
     cfg->mode = 1;
-  else if (cfg->mode == 1)
+    // the rest is its own sparse matrix: the decider's mode-0 knobs for its
+    // features (a TMA-gather label, mode 2, has no W / F / G for mode 0)
+    pspmm_config rc{};
+    if (A->dense->rest_f_ok && pspmm_decide_config(&A->dense->rest_f, K, &rc) == PSPMM_OK &&
+        rc.mode != 2 && rc.F >= 1) {
+      cfg->W = rc.W;
+      cfg->F = rc.F;
+      cfg->G = rc.G;
+      cfg->order = rc.order;
+    }
+  } else if (cfg->mode == 1)
     cfg->mode = 0;
   return PSPMM_OK;
 }

@@ -28,6 +28,8 @@ struct DenseTiles {
   int32_t *d_panel = nullptr;      // num_panels: 128-row panel index
   int32_t *d_tile_col = nullptr;   // num_tiles: first column of the tile
   pspmm_pcsr_s *rest = nullptr;    // A minus the dense tiles (same V, S, omega)
+  pspmm_features rest_f{};         // Table-3 features of the rest
+  bool rest_f_ok = false;
 };
 struct pspmm_pcsr_s {
   int64_t n_rows = 0, n_cols = 0, num_panels = 0, nnz = 0, nnz_v = 0, num_chunks = 0;

@@ -528,7 +528,12 @@ pspmm_status attach_dense(pspmm_pcsr_s *A, const int32_t *d_rowptr, const int32_
   // gives the same (empty) chunks, so force omega there
   st = build_pcsr(n, A->n_cols, rn, d_rrp, d_rci, d_rvl, A->V, A->S, A->omega,
                   rn == 0 ? A->omega : 0, stream, D->rest);
-  PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
+  // Table-3 features of the rest (a different sparse matrix from A), for
+  // pspmm_decide_dense to pick the rest's engine knobs
+  if (st == PSPMM_OK && rn > 0 && A->n_cols == n &&
+      compute_features(n, rn, d_rrp, d_rci, 32, stream, &D->rest_f) == PSPMM_OK)
+    D->rest_f_ok = true;
+  if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return fail(e, "pcsr_attach_dense");
   cudaFree(d_rrp);
   cudaFree(d_rci);
   cudaFree(d_rvl);

@@ -172,3 +172,33 @@ def test_empty_matrix_mode1():
     A.run(B, C, api.Config(W=2, F=1, mode=1))
     torch.cuda.synchronize()
     assert float(C.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("kind", ["community", "uniform"])
+def test_decide_dense_rule(kind):
+    """pspmm_decide_dense: mode 1 iff the >= 10 %-dense tiles hold >= 5 % of
+    the nonzeros; the decided config (rest knobs from the rest's features)
+    matches the oracle."""
+    import torch
+    from paper_2605_15695_b200 import api
+    g = _community(4096, 512, 80, 0.7, seed=21) if kind == "community" else \
+        gen.uniform(4096, 40, 22)
+    K = 64
+    rp, ci, vl = dev(g)
+    cfg = api.auto_config(g.n, g.nnz, rp, ci, K)
+    A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, cfg.V, cfg.S)
+    cfg2, info = api.auto_dense(A, rp, ci, vl, K, cfg)
+    thr = int(np.ceil(0.1 * 4096))
+    _, tiles, nnz_dense = _tile_counts(g, thr)
+    assert info["num_tiles"] == tiles and info["nnz_dense"] == nnz_dense
+    assert (cfg2.mode == 1) == (tiles > 0 and nnz_dense >= 0.05 * g.nnz)
+    assert cfg2.mode == (1 if kind == "community" else cfg.mode)
+    assert (cfg2.V, cfg2.S) == (cfg.V, cfg.S)
+    B = gen.dense(g.n, K, 3)
+    C = torch.full((g.n, K), float("nan"), device="cuda")
+    A.run(torch.from_numpy(B).cuda(), C, cfg2)
+    torch.cuda.synchronize()
+    ref, mag = oracle_ref(g, B)
+    assert_parity(C.cpu().numpy(), ref, mag, f"decided {cfg2}")
+    # K % 16 != 0 never takes mode 1
+    assert api.pspmm_decide_dense(A, 40, 0.05, cfg).mode != 1
