@@ -181,7 +181,7 @@ def test_decide_dense_rule(kind):
     matches the oracle."""
     import torch
     from paper_2605_15695_b200 import api
-    g = _community(4096, 512, 80, 0.7, seed=21) if kind == "community" else \
+    g = _community(4096, 512, 120, 0.8, seed=21) if kind == "community" else \
         gen.uniform(4096, 40, 22)
     K = 64
     rp, ci, vl = dev(g)
