@@ -178,10 +178,172 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
   if (a.fan.n) __threadfence_system();
 }
 
+
+// Ring form (PSPMM_SHORT_RING = 1): the same row-strided schedule, but the B
+// rows of the next row are copied into a lane-private shared-memory slot with
+// cp.async (LDGSTS) while the current row is consumed from the other slot.
+// In-flight gathers then cost no registers, so two rows per group stay in
+// flight at any time (the register form holds one and stalls on it).
+// Slot layout: [warp][slot][item = u F + f][lane] float4 (conflict-free).
+#ifndef PSPMM_SHORT_RING
+#define PSPMM_SHORT_RING 0  // A/B: the ring form measured slower (profiles/r01/mode3_ab/README.md, ab4)
+#endif
+
+#ifndef PSPMM_SHORT_RING_CG
+#define PSPMM_SHORT_RING_CG 0  // 1: cp.async.cg (L2 only) instead of .ca (L1-allocating)
+#endif
+__device__ __forceinline__ void cp_async16(float4 *dst, const float4 *src) {
+#if PSPMM_SHORT_RING_CG
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+  return;
+#endif
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+template <int F, int G>
+__global__ void __launch_bounds__(256) spmm_ring_kernel(const ShortArgs a) {
+  constexpr int U = (8 / F) < G ? (8 / F) : G;  // vectors staged per row
+  constexpr int ITEMS = U * F;                  // float4 per lane per slot
+  extern __shared__ float4 ring_smem[];
+  const int lane = threadIdx.x & 31;
+  const int g = lane / G, l = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
+  const int groups = (int)((gridDim.x * blockDim.x) >> 5) * (32 / G);
+  float4 *slot0 = ring_smem + (size_t)(threadIdx.x >> 5) * (2 * ITEMS * 32) + lane;
+  const int col0 = blockIdx.y * G * F * 4;
+  bool cok[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) cok[f] = col0 + (f * G + l) * 4 < a.K;
+  const float4 *bl = reinterpret_cast<const float4 *>(a.B + col0 + l * 4);
+  const uint32_t ldq = (uint32_t)(a.ldb / 4);
+  const int32_t *__restrict__ rowptr = a.rowptr;
+  const int32_t *__restrict__ colidx = a.colidx;
+  const float *__restrict__ val = a.val;
+  const int row_end = a.row_end;
+  int r = a.row_begin + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G) + g;
+
+  // issue the staged gathers of one row (its first U vectors) into slot s
+  auto stage = [&](int s, int h, int t, int c) {
+    const int cnt = t - h;
+    float4 *dst = slot0 + s * (ITEMS * 32);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int cu = __shfl_sync(gmask, c, u, G);
+      if (u < cnt) {
+        const float4 *row = bl + (uint32_t)cu * ldq;
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+          if (cok[f]) cp_async16(dst + (u * F + f) * 32, row + f * G);
+      }
+    }
+    cp_async_commit();
+  };
+
+  // pipeline registers: rowPtr of rows k, k+1, k+2; vectors of rows k, k+1
+  int h0 = 0, t0 = 0, h1 = 0, t1 = 0, h2 = 0, t2 = 0;
+  if (r < row_end) { h0 = rowptr[r]; t0 = rowptr[r + 1]; }
+  if (r + groups < row_end) { h1 = rowptr[r + groups]; t1 = rowptr[r + groups + 1]; }
+  if (r + 2 * groups < row_end) { h2 = rowptr[r + 2 * groups]; t2 = rowptr[r + 2 * groups + 1]; }
+  int c0 = 0, c1 = 0;
+  float v0 = 0.f, v1 = 0.f;
+  if (h0 + l < t0) { c0 = lda(colidx + h0 + l); v0 = lda(val + h0 + l); }
+  if (h1 + l < t1) { c1 = lda(colidx + h1 + l); v1 = lda(val + h1 + l); }
+  stage(0, h0, t0, c0);
+  int s = 0;
+  for (; r < row_end; r += groups) {
+    // row k + 1 into the other slot, then prefetch row k + 2's vectors and
+    // row k + 3's rowPtr
+    stage(s ^ 1, h1, t1, c1);
+    int c2 = 0;
+    float v2 = 0.f;
+    if (h2 + l < t2) { c2 = lda(colidx + h2 + l); v2 = lda(val + h2 + l); }
+    const int r3 = r + 3 * groups;
+    int h3 = 0, t3 = 0;
+    if (r3 < row_end) { h3 = rowptr[r3]; t3 = rowptr[r3 + 1]; }
+    // consume row k (its group of copies is the older of the two in flight)
+    cp_async_wait1();
+    const int cnt = t0 - h0;
+    const float4 *src = slot0 + s * (ITEMS * 32);
+    float4 acc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) acc[f] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float vu = __shfl_sync(gmask, v0, u, G);
+      if (u < cnt)
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+          if (cok[f]) fma4(acc[f], vu, src[(u * F + f) * 32]);
+    }
+    for (int j = U; j < cnt; ++j) {  // the rest of a long row: direct loads
+      int c;
+      float v;
+      if (j < G) {
+        c = __shfl_sync(gmask, c0, j, G);
+        v = __shfl_sync(gmask, v0, j, G);
+      } else {
+        c = lda(colidx + h0 + j);
+        v = lda(val + h0 + j);
+      }
+      const float4 *row = bl + (uint32_t)c * ldq;
+#pragma unroll
+      for (int f = 0; f < F; ++f)
+        if (cok[f]) fma4(acc[f], v, __ldg(row + f * G));
+    }
+    float4 *crow = reinterpret_cast<float4 *>(a.C + (int64_t)r * a.ldc + col0 + l * 4);
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+      if (cok[f]) {
+        float4 v = acc[f];
+        if (a.accumulate) {
+          const float4 o = crow[f * G];
+          v.x += o.x;
+          v.y += o.y;
+          v.z += o.z;
+          v.w += o.w;
+        }
+        __stcs(crow + f * G, v);
+#pragma unroll 1
+        for (int d = 0; d < a.fan.n; ++d)
+          __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + (int64_t)r * a.ldc + col0 + l * 4) +
+                     f * G,
+                 v);
+      }
+    h0 = h1; t0 = t1; c0 = c1; v0 = v1;
+    h1 = h2; t1 = t2; c1 = c2; v1 = v2;
+    h2 = h3; t2 = t3;
+    s ^= 1;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (a.fan.n) __threadfence_system();
+}
+
 using ShortFn = void (*)(const ShortArgs);
 
 template <int F>
 ShortFn pick_g(int G) {
+#if PSPMM_SHORT_RING
+  switch (G) {
+    case 2: return spmm_ring_kernel<F, 2>;
+    case 4: return spmm_ring_kernel<F, 4>;
+    case 8: return spmm_ring_kernel<F, 8>;
+    case 16: return spmm_ring_kernel<F, 16>;
+    case 32: return spmm_ring_kernel<F, 32>;
+    default: return nullptr;
+  }
+#else
   switch (G) {
     case 2: return spmm_short_kernel<F, 2>;
     case 4: return spmm_short_kernel<F, 4>;
@@ -190,6 +352,7 @@ ShortFn pick_g(int G) {
     case 32: return spmm_short_kernel<F, 32>;
     default: return nullptr;
   }
+#endif
 }
 
 ShortFn pick(int F, int G) {
@@ -243,12 +406,24 @@ pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb
   args.fan = fan;
   const int threads = std::min(cfg.W, 8) * 32;
   const int64_t per_block = threads / 32 * (32 / G);
+  int64_t bx = (u1 - u0 + per_block - 1) / per_block;
+#if PSPMM_SHORT_RING
+  // two slots of (U F) float4 per lane; one wave of resident blocks
+  const int U = std::min(8 / F, G);
+  const int smem = threads * 2 * U * F * 16;
+  PSPMM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  PSPMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+  if (per_sm < 1) PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run mode 3: no resident block");
+  bx = std::min<int64_t>(bx, (int64_t)num_sms() * per_sm * PSPMM_SHORT_WAVES);
+#else
+  const int smem = 0;
   // a few waves of resident blocks (launch bounds: 256 x PSPMM_SHORT_MINB threads / SM)
   const int64_t resident = std::max<int64_t>(1, 256 * PSPMM_SHORT_MINB / threads);
-  int64_t bx = (u1 - u0 + per_block - 1) / per_block;
   bx = std::min<int64_t>(bx, (int64_t)num_sms() * resident * PSPMM_SHORT_WAVES);
+#endif
   const int64_t by = (K + 4 * G * F - 1) / (4 * G * F);
-  fn<<<dim3((unsigned)bx, (unsigned)by), threads, 0, stream>>>(args);
+  fn<<<dim3((unsigned)bx, (unsigned)by), threads, smem, stream>>>(args);
   PSPMM_CUDA_TRY(cudaGetLastError());
   return PSPMM_OK;
 }
