@@ -83,6 +83,17 @@ inline int num_sms() {
   return sms;
 }
 
+inline int64_t l2_bytes() {
+  static int64_t l2 = 0;
+  if (!l2) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+    l2 = v > 0 ? v : (int64_t)126 << 20;
+  }
+  return l2;
+}
+
 // validate.cu
 pspmm_status validate_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t *d_rowptr,
                           const int32_t *d_colidx, cudaStream_t stream);

@@ -30,7 +30,11 @@ __global__ void zero_all_kernel(int64_t n_rows, int32_t K, float *__restrict__ C
     C[(t / K) * ldc + t % K] = 0.f;
 }
 
-KernelFn pick_kernel(int V, int S, bool vec, int F, int G) {
+KernelFn pick_kernel(int V, int S, bool vec, int F, int G, bool na) {
+  if (vec && na) {
+    if (V == 1) return S ? pick_v1s1_na(F, G) : pick_v1s0_na(F, G);
+    return S ? pick_v2s1_na(F, G) : pick_v2s0_na(F, G);
+  }
   if (V == 1) return S ? pick_v1s1(vec, F, G) : pick_v1s0(vec, F, G);
   return S ? pick_v2s1(vec, F, G) : pick_v2s0(vec, F, G);
 }
@@ -110,7 +114,10 @@ pspmm_status make_plan(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int
     G = ceil_pow2(K);
     cols_per_pass = G;
   }
-  plan->fn = pick_kernel(A->V, A->S, vec, F, G);
+  // B far larger than L2 (> 2x): its gathers cannot hit in L1, so they skip
+  // L1 allocation (A/B: products-shaped -5 %)
+  const bool na = (double)A->n_cols * (double)ldb * 4.0 > 2.0 * (double)l2_bytes();
+  plan->fn = pick_kernel(A->V, A->S, vec, F, G, na);
   if (!plan->fn) PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: no kernel instance for this config");
   plan->threads = cfg.W * 32;
   plan->G = G;

@@ -1,0 +1,9 @@
+// Kernel instances of the engine for V = 2, S = 0 with L1::no_allocate B
+// gathers (see spmm_kernel.cuh).
+#include "spmm_kernel.cuh"
+
+namespace pspmm {
+namespace detail {
+KernelFn pick_v2s0_na(int F, int G) { return pick_na<2, 0>(F, G); }
+}  // namespace detail
+}  // namespace pspmm

@@ -70,10 +70,19 @@ __device__ __forceinline__ float ld_a(const float *p, uint64_t pol) {
                : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
+// B gathers: L1-allocating, or (NA) L1::no_allocate — for B far larger than
+// L2, whose gathers cannot hit in L1 (the allocations only thrash it); the
+// NA instances are separate kernels (spmm_inst_*_na.cu), chosen per launch
+template <bool NA>
 __device__ __forceinline__ void ld_b(float4 &v, const char *p, uint64_t pol) {
-  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  if constexpr (NA)
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  else
+    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
 }
+template <bool NA>
 __device__ __forceinline__ void ld_b(float &v, const char *p, uint64_t pol) {
   asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
 }
@@ -161,7 +170,7 @@ __device__ __forceinline__ void load_tile(const SpmmArgs &a, int base, int tail,
 // the tile exists (no per-vector predicates).
 // One batch: U vectors starting at tile position j0 (J0 is j0 when it is a
 // compile-time constant, -1 when the batch loop is rolled; then M == 1).
-template <int V, int F, int G, int M, int U, bool VEC, bool FULL, typename T>
+template <int V, int F, int G, int M, int U, bool VEC, bool FULL, bool NA, typename T>
 __device__ __forceinline__ void mac_batch(const char *__restrict__ bptr, uint32_t stride,
                                           const bool (&cok)[F], unsigned gmask, int cnt,
                                           uint64_t pol, const int (&mc)[M],
@@ -180,7 +189,7 @@ __device__ __forceinline__ void mac_batch(const char *__restrict__ bptr, uint32_
 #pragma unroll
     for (int f = 0; f < F; ++f) {
       if ((FULL || j < cnt) && cok[f])
-        ld_b(b[u][f], row + f * FSTEP, pol);
+        ld_b<NA>(b[u][f], row + f * FSTEP, pol);
       else
         b[u][f] = zero_v<T>();
     }
@@ -204,7 +213,7 @@ __device__ __forceinline__ void mac_batch(const char *__restrict__ bptr, uint32_
 #define PSPMM_INFLIGHT 8
 #endif
 
-template <int V, int F, int G, int M, int U, bool VEC, bool FULL, typename T>
+template <int V, int F, int G, int M, int U, bool VEC, bool FULL, bool NA, typename T>
 __device__ __forceinline__ void mac_tile(const char *__restrict__ bptr, uint32_t stride,
                                          const bool (&cok)[F], unsigned gmask, int cnt,
                                          uint64_t pol, const int (&mc)[M],
@@ -214,13 +223,13 @@ __device__ __forceinline__ void mac_tile(const char *__restrict__ bptr, uint32_t
 #pragma unroll 1
     for (int j0 = 0; j0 < TILE; j0 += U) {
       if (FULL || j0 < cnt)
-        mac_batch<V, F, G, M, U, VEC, FULL>(bptr, stride, cok, gmask, cnt, pol, mc, mv, acc, j0);
+        mac_batch<V, F, G, M, U, VEC, FULL, NA>(bptr, stride, cok, gmask, cnt, pol, mc, mv, acc, j0);
     }
   } else {
 #pragma unroll
     for (int j0 = 0; j0 < TILE; j0 += U) {
       if (FULL || j0 < cnt)  // uniform inside the group
-        mac_batch<V, F, G, M, U, VEC, FULL>(bptr, stride, cok, gmask, cnt, pol, mc, mv, acc, j0);
+        mac_batch<V, F, G, M, U, VEC, FULL, NA>(bptr, stride, cok, gmask, cnt, pol, mc, mv, acc, j0);
     }
   }
 }
@@ -241,7 +250,7 @@ __device__ __forceinline__ void mac_tile(const char *__restrict__ bptr, uint32_t
 #define PSPMM_WAVES 0
 #endif
 
-template <int V, int S, int F, int G, bool VEC>
+template <int V, int S, int F, int G, bool VEC, bool NA = false>
 __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
     spmm_kernel(const SpmmArgs a) {
   using T = typename std::conditional<VEC, float4, float>::type;
@@ -305,9 +314,9 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
     if (more) load_tile<V, M, G>(a, base + TILE, tail, l, pol_a, nc, nv);
     const int cnt = tail - base;
     if (cnt >= TILE)
-      mac_tile<V, F, G, M, U, VEC, true>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
+      mac_tile<V, F, G, M, U, VEC, true, NA>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
     else
-      mac_tile<V, F, G, M, U, VEC, false>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
+      mac_tile<V, F, G, M, U, VEC, false, NA>(bptr, stride, cok, gmask, cnt, pol_b, mc, mv, acc);
     if (more) {
 #pragma unroll
       for (int m = 0; m < M; ++m) {
@@ -348,15 +357,15 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
 
 using KernelFn = void (*)(const SpmmArgs);
 
-template <int V, int S, int F, bool VEC>
+template <int V, int S, int F, bool VEC, bool NA = false>
 KernelFn pick_g(int G) {
   switch (G) {
-    case 1: return spmm_kernel<V, S, F, 1, VEC>;
-    case 2: return spmm_kernel<V, S, F, 2, VEC>;
-    case 4: return spmm_kernel<V, S, F, 4, VEC>;
-    case 8: return spmm_kernel<V, S, F, 8, VEC>;
-    case 16: return spmm_kernel<V, S, F, 16, VEC>;
-    case 32: return spmm_kernel<V, S, F, 32, VEC>;
+    case 1: return spmm_kernel<V, S, F, 1, VEC, NA>;
+    case 2: return spmm_kernel<V, S, F, 2, VEC, NA>;
+    case 4: return spmm_kernel<V, S, F, 4, VEC, NA>;
+    case 8: return spmm_kernel<V, S, F, 8, VEC, NA>;
+    case 16: return spmm_kernel<V, S, F, 16, VEC, NA>;
+    case 32: return spmm_kernel<V, S, F, 32, VEC, NA>;
     default: return nullptr;
   }
 }
@@ -377,11 +386,31 @@ KernelFn pick(bool vec, int F, int G) {
   }
 }
 
-// one per (V, S) translation unit
+// the 128-bit instances with L1::no_allocate B gathers
+template <int V, int S>
+KernelFn pick_na(int F, int G) {
+  switch (F) {
+    case 1: return pick_g<V, S, 1, true, true>(G);
+    case 2: return pick_g<V, S, 2, true, true>(G);
+    case 3: return pick_g<V, S, 3, true, true>(G);
+    case 4: return pick_g<V, S, 4, true, true>(G);
+    case 5: return pick_g<V, S, 5, true, true>(G);
+    case 6: return pick_g<V, S, 6, true, true>(G);
+    case 7: return pick_g<V, S, 7, true, true>(G);
+    case 8: return pick_g<V, S, 8, true, true>(G);
+    default: return nullptr;
+  }
+}
+
+// one per (V, S) translation unit, and one per (V, S) for the NA instances
 KernelFn pick_v1s0(bool vec, int F, int G);
 KernelFn pick_v1s1(bool vec, int F, int G);
 KernelFn pick_v2s0(bool vec, int F, int G);
 KernelFn pick_v2s1(bool vec, int F, int G);
+KernelFn pick_v1s0_na(int F, int G);
+KernelFn pick_v1s1_na(int F, int G);
+KernelFn pick_v2s0_na(int F, int G);
+KernelFn pick_v2s1_na(int F, int G);
 
 }  // namespace detail
 }  // namespace pspmm
