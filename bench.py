@@ -506,7 +506,7 @@ def main():
                     r = measure_single(gg, args.steps, args.warmup, flush, stream,
                                        want_cusparse=not args.no_cusparse, want_e2e=False)
                 r["roofline_frac"] = r["achieved_gbs"] / peak
-                r.pop("features", None)
+                # realised Table-3 features of every workload stay in the line
                 per.append(r)
                 del gg
             line["per_config"] = per
