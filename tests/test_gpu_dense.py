@@ -202,3 +202,30 @@ def test_decide_dense_rule(kind):
     assert_parity(C.cpu().numpy(), ref, mag, f"decided {cfg2}")
     # K % 16 != 0 never takes mode 1
     assert api.pspmm_decide_dense(A, 40, 0.05, cfg).mode != 1
+
+
+def test_host_entries_mode1():
+    """The host entries run mode 1 whole: pspmm_spmm_run_host and the batch
+    entry (3 products through two rotating buffer sets)."""
+    import torch
+    from paper_2605_15695_b200 import api
+    g = _community(2000, 256, 60, 0.7, seed=31)
+    K = 32
+    rp, ci, vl = dev(g)
+    A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, 1, 0)
+    info = api.pspmm_pcsr_attach_dense(A, rp, ci, vl, 0.05, k_max=K)
+    assert info["num_tiles"] > 0
+    cfg = api.Config(W=2, F=1, mode=1)
+    Bs = [gen.dense(g.n, K, 40 + i) for i in range(3)]
+    hB = [torch.from_numpy(b).pin_memory() for b in Bs]
+    hC = [torch.full((g.n, K), float("nan")).pin_memory() for _ in Bs]
+    dB = [torch.empty((g.n, K), device="cuda") for _ in range(2)]
+    dC = [torch.empty((g.n, K), device="cuda") for _ in range(2)]
+    api.pspmm_spmm_run_host_batch(A, hB, hC, cfg, dB, dC)
+    for b, c in zip(Bs, hC):
+        ref, mag = oracle_ref(g, b)
+        assert_parity(c.numpy(), ref, mag, "host batch mode 1")
+    h1 = torch.full((g.n, K), float("nan")).pin_memory()
+    api.pspmm_spmm_run_host(A, hB[0], h1, cfg, dB[0], dC[0])
+    ref, mag = oracle_ref(g, Bs[0])
+    assert_parity(h1.numpy(), ref, mag, "host mode 1")
