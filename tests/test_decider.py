@@ -55,6 +55,9 @@ def ceil_pow2(x):
     return p
 
 
+L2_B200 = 132644864.0  # decide.cpp kL2Bytes
+
+
 def test_c_decider_evaluates_the_header_tree():
     from paper_2605_15695_b200 import api
     model = parse_header()
@@ -72,6 +75,12 @@ def test_c_decider_evaluates_the_header_tree():
         K = int(rng.choice([8, 16, 32, 48, 64, 96, 128, 160, 256]))
         mode, V, S, W, F, P, order = walk(model, f, K)
         c = api.pspmm_decide_config(f, K)
+        q = (K + 3) // 4
+        G = ceil_pow2(-(-q // (F * P))) if mode != 2 else 0
+        if mode == 0 and -(-K // (4 * G * F)) > 1 and n * K * 4 > 2 * L2_B200 and -(-q // 32) <= 8:
+            # the single-pass guard for B far beyond L2 (decide.cpp)
+            F = -(-q // 32)
+            G = ceil_pow2(-(-q // F))
         if mode == 2 and K % 32 == 0:
             assert (c.mode, c.V, c.S, c.W) == (2, V, S, W)
         elif mode in (3, 4) and K % 4 == 0:
@@ -79,9 +88,21 @@ def test_c_decider_evaluates_the_header_tree():
         else:
             assert (c.mode, c.V, c.S, c.W) == (0, V, S, W)
             if mode == 0:
-                q = (K + 3) // 4
-                assert c.F == F and c.G == ceil_pow2(-(-q // (F * P)))
+                assert c.F == F and c.G == G
                 assert c.order == order
+
+
+def test_single_pass_guard():
+    """B far beyond L2 (n K 4 > 2 x L2): whatever the forest says, one column
+    pass of up to 32 lanes; below that size the forest's passes stand."""
+    from paper_2605_15695_b200 import api
+    f = dict(n=2449029.0, n_hat=2449029.0, nnz=123718280.0, delta=1.0, d=50.5, d_hat=50.5,
+             d_max=17425.0, cv=1.08, cv_hat=1.08, sr1=1.23, sr2=1.2, rho=2.06e-5, b=2.3e6,
+             b_max=2449010.0, pr1=0.0, pr2=0.5)
+    for K in (128, 256, 512):
+        c = api.pspmm_decide_config(f, K)
+        if c.mode == 0:
+            assert -(-K // (4 * c.G * c.F)) == 1, (K, c)
 
 
 def test_trainer_recovers_planted_rule():
