@@ -91,6 +91,11 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
   c.order = c.mode == 0 ? lab[6] : 0;
   if (c.mode == 2 && K % 32 != 0) c.mode = 0;  // TMA engine needs K % 32 == 0
   if ((c.mode == 3 || c.mode == 4) && K % 4 != 0) c.mode = 0;  // short-row engines: 128-bit only
+  // the short-row engines walk a row's vectors beyond the staged window one
+  // dependent load at a time: a hub row serialises its group (K sweep,
+  // Cora K = 128, mode 3 0.059 ms vs cuSPARSE 0.023), so
+  // graphs with rows longer than 64 vectors stay on mode 0
+  if ((c.mode == 3 || c.mode == 4) && f->d_max > 64.0) c.mode = 0;
   if (c.mode == 2) {
     pick_fg(K, 0, &c.F, &c.G);  // unused by mode 2; a valid mode-0 fallback
   } else if (lab[0] == 2) {

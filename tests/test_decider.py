@@ -74,6 +74,8 @@ def test_c_decider_evaluates_the_header_tree():
                  pr2=rng.uniform(0, 0.5))
         K = int(rng.choice([8, 16, 32, 48, 64, 96, 128, 160, 256]))
         mode, V, S, W, F, P, order = walk(model, f, K)
+        if mode in (3, 4) and f["d_max"] > 64:  # hub-row guard (decide.cpp)
+            mode = 0
         c = api.pspmm_decide_config(f, K)
         q = (K + 3) // 4
         G = ceil_pow2(-(-q // (F * P))) if mode != 2 else 0
