@@ -96,6 +96,12 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
   // Cora K = 128, mode 3 0.059 ms vs cuSPARSE 0.023), so
   // graphs with rows longer than 64 vectors stay on mode 0
   if ((c.mode == 3 || c.mode == 4) && f->d_max > 64.0) c.mode = 0;
+  // vectorized blocking only where it saves B reads: at PR_2 ~ 0.5 a V = 2
+  // vector is a padded single value (the paper's T1: V = 2 loses
+  // at PR 47.8-49 %); the forest's V = 2 there extrapolates a noise-level
+  // label (products K = 128) to other graphs (Reddit K = 128: 4.46 ms with
+  // V = 2 vs 3.22 ms with V = 1)
+  if (c.V == 2 && f->pr2 >= 0.45) c.V = 1;
   if (c.mode == 2) {
     pick_fg(K, 0, &c.F, &c.G);  // unused by mode 2; a valid mode-0 fallback
   } else if (lab[0] == 2) {

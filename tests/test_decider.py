@@ -76,6 +76,8 @@ def test_c_decider_evaluates_the_header_tree():
         mode, V, S, W, F, P, order = walk(model, f, K)
         if mode in (3, 4) and f["d_max"] > 64:  # hub-row guard (decide.cpp)
             mode = 0
+        if V == 2 and f["pr2"] >= 0.45:  # padding guard (decide.cpp)
+            V = 1
         c = api.pspmm_decide_config(f, K)
         q = (K + 3) // 4
         G = ceil_pow2(-(-q // (F * P))) if mode != 2 else 0
