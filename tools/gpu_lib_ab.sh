@@ -1,5 +1,6 @@
 #!/bin/bash
 # A/B of library variants on the decided configs: main vs $VARIANTS, two
+# (build each variant first, e.g. python tools/variants.py git:HEAD~1=prev)
 # alternating rounds.  usage: VARIANTS="bnoalloc" bash tools/gpu_lib_ab.sh
 export PSPMM_GEN_CACHE=/tmp/pspmm_gen_cache
 O=gpurun_out; mkdir -p $O

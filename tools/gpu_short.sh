@@ -1,4 +1,5 @@
 #!/bin/bash
+# (build the variant libraries first: python tools/variants.py shortreg=PSPMM_SHORT_RING=0 ringcg=PSPMM_SHORT_RING=1,PSPMM_SHORT_RING_CG=1; main is then the register form)
 # Engine mode 3 A/B: the cp.async ring form (main, .ca), the ring with .cg
 # (variant ringcg) and the register form (variant shortreg): roadNet sweep
 # per library, plus one ncu capture of the ring form.
