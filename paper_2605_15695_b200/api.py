@@ -459,7 +459,15 @@ def pspmm_spmm_run_host(A: Pcsr, hB, hC, cfg: Config, dB, dC, stream=None):
         return t.ctypes.data_as(_P), t.shape[1]
 
     hb, K = hptr(hB)
-    hc, _ = hptr(hC)
+    hc, Kc = hptr(hC)
+    # the C side copies n_cols x ldb floats from hB and n_rows x ldc into hC:
+    # host and device shapes must agree exactly (no padded staging buffers)
+    if tuple(hB.shape) != (A.n_cols, K) or hC.shape[0] < A.n_rows or Kc != K:
+        raise ValueError(f"run_host: need hB ({A.n_cols}, K) and hC (>= {A.n_rows}, K); got "
+                         f"{tuple(hB.shape)} / {tuple(hC.shape)}")
+    for t, name, rows in ((dB, "dB", A.n_cols), (dC, "dC", A.n_rows)):
+        if not (t.is_contiguous() and t.dim() == 2 and t.shape[1] == K and t.shape[0] >= rows):
+            raise ValueError(f"run_host: {name} must be contiguous (>= {rows}, {K})")
     db, ldb = _dense(dB, "dB")
     dc, ldc = _dense(dC, "dC")
     _check(_lib.pspmm_spmm_run_host(A.handle, hb, ldb, K, hc, ldc, cfg, db, dc, _stream(stream)),

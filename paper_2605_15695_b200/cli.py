@@ -74,7 +74,7 @@ def read_mtx(path):
 
 
 def coo_to_csr(r, c, v, nr, nc):
-    """Sort by (row, col), sum duplicates -> canonical CSR (int32 / fp32)."""
+    """Sort by (row, col), sum duplicates, drop zeros -> canonical CSR (int32 / fp32)."""
     if nr >= 2**31 or nc >= 2**31 or len(r) >= 2**31:
         raise InputError("matrix exceeds int32 indexing")
     order = np.lexsort((c, r))
@@ -85,6 +85,10 @@ def coo_to_csr(r, c, v, nr, nc):
         idx = np.cumsum(new) - 1
         v = np.bincount(idx, weights=v, minlength=int(idx[-1]) + 1)
         r, c = r[new], c[new]
+        # explicit zeros (and duplicates summing to zero) are not stored
+        # (SPEC load_matrix_market): they would inflate nnz and the features
+        keep = v != 0
+        r, c, v = r[keep], c[keep], v[keep]
     rowptr = np.zeros(nr + 1, np.int64)
     np.cumsum(np.bincount(r, minlength=nr), out=rowptr[1:])
     return (rowptr.astype(np.int32), c.astype(np.int32), v.astype(np.float32), nr, nc)

@@ -14,7 +14,19 @@ namespace pspmm {
 
 static thread_local std::string g_last_error;
 
-void set_error(const std::string &msg) { g_last_error = msg; }
+void set_error(const std::string &msg) {
+  try {
+    g_last_error = msg;
+  } catch (...) {  // never throws: the message is best-effort
+  }
+}
+
+void set_error_cstr(const char *where, const char *what) noexcept {
+  try {
+    g_last_error = std::string(where) + ": " + what;
+  } catch (...) {
+  }
+}
 
 pspmm_status cuda_status(cudaError_t e, const char *where) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
@@ -67,88 +79,100 @@ const char *pspmm_version(void) { return "pspmm 0.1 sm_100a"; }
 pspmm_status pspmm_csr_validate_rect(int64_t n_rows, int64_t n_cols, int64_t nnz,
                                      const int32_t *d_rowptr, const int32_t *d_colidx,
                                      void *stream) {
-  return validate_csr(n_rows, n_cols, nnz, d_rowptr, d_colidx, as_stream(stream));
+  return pspmm::guarded("csr_validate_rect", [&]() -> pspmm_status {
+    return validate_csr(n_rows, n_cols, nnz, d_rowptr, d_colidx, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_csr_validate(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                                 const int32_t *d_colidx, void *stream) {
-  return validate_csr(n, n, nnz, d_rowptr, d_colidx, as_stream(stream));
+  return pspmm::guarded("csr_validate", [&]() -> pspmm_status {
+    return validate_csr(n, n, nnz, d_rowptr, d_colidx, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_pcsr_build_rect(int64_t n_rows, int64_t n_cols, int64_t nnz,
                                    const int32_t *d_rowptr, const int32_t *d_colidx,
                                    const float *d_val, int32_t V, int32_t S, int32_t omega,
                                    int32_t sg_override, void *stream, pspmm_pcsr *out) {
-  if (!out) {
-    set_error("pcsr_build: null out");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  *out = nullptr;
-  pspmm_pcsr_s *A = new (std::nothrow) pspmm_pcsr_s();
-  if (!A) {
-    set_error("pcsr_build: host allocation failed");
-    return PSPMM_ERR_OOM;
-  }
-  pspmm_status st = build_pcsr(n_rows, n_cols, nnz, d_rowptr, d_colidx, d_val, V, S, omega,
-                               sg_override, as_stream(stream), A);
-  if (st != PSPMM_OK) {
-    pspmm_pcsr_destroy(A);
-    return st;
-  }
-  *out = A;
-  return PSPMM_OK;
+  return pspmm::guarded("pcsr_build_rect", [&]() -> pspmm_status {
+    if (!out) {
+      set_error("pcsr_build: null out");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    *out = nullptr;
+    pspmm_pcsr_s *A = new (std::nothrow) pspmm_pcsr_s();
+    if (!A) {
+      set_error("pcsr_build: host allocation failed");
+      return PSPMM_ERR_OOM;
+    }
+    pspmm_status st = build_pcsr(n_rows, n_cols, nnz, d_rowptr, d_colidx, d_val, V, S, omega,
+                                 sg_override, as_stream(stream), A);
+    if (st != PSPMM_OK) {
+      pspmm_pcsr_destroy(A);
+      return st;
+    }
+    *out = A;
+    return PSPMM_OK;
+  });
 }
 
 pspmm_status pspmm_pcsr_build(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                               const int32_t *d_colidx, const float *d_val, int32_t V, int32_t S,
                               int32_t omega, int32_t sg_override, void *stream, pspmm_pcsr *out) {
-  return pspmm_pcsr_build_rect(n, n, nnz, d_rowptr, d_colidx, d_val, V, S, omega, sg_override,
-                               stream, out);
+  return pspmm::guarded("pcsr_build", [&]() -> pspmm_status {
+    return pspmm_pcsr_build_rect(n, n, nnz, d_rowptr, d_colidx, d_val, V, S, omega, sg_override,
+                                 stream, out);
+  });
 }
 
 pspmm_status pspmm_pcsr_get_info(pspmm_pcsr A, pspmm_pcsr_info *out) {
-  if (!A || !out) {
-    set_error("pcsr_get_info: null argument");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  std::memset(out, 0, sizeof(*out));
-  out->n = A->n_rows;
-  out->num_panels = A->num_panels;
-  out->nnz = A->nnz;
-  out->nnz_v = A->nnz_v;
-  out->num_chunks = A->num_chunks;
-  out->sg = A->sg;
-  out->V = A->V;
-  out->S = A->S;
-  out->omega = A->omega;
-  out->pr = A->pr;
-  out->sr = A->sr;
-  return PSPMM_OK;
+  return pspmm::guarded("pcsr_get_info", [&]() -> pspmm_status {
+    if (!A || !out) {
+      set_error("pcsr_get_info: null argument");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    std::memset(out, 0, sizeof(*out));
+    out->n = A->n_rows;
+    out->num_panels = A->num_panels;
+    out->nnz = A->nnz;
+    out->nnz_v = A->nnz_v;
+    out->num_chunks = A->num_chunks;
+    out->sg = A->sg;
+    out->V = A->V;
+    out->S = A->S;
+    out->omega = A->omega;
+    out->pr = A->pr;
+    out->sr = A->sr;
+    return PSPMM_OK;
+  });
 }
 
 pspmm_status pspmm_pcsr_export(pspmm_pcsr A, int32_t *h_rowptr, int32_t *h_colidx, float *h_val,
                                int32_t *h_trow) {
-  if (!A) {
-    set_error("pcsr_export: null handle");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  if (h_rowptr)
-    PSPMM_CUDA_TRY(cudaMemcpy(h_rowptr, A->d_rowptr, (size_t)A->rowptr_len * sizeof(int32_t),
-                              cudaMemcpyDeviceToHost));
-  if (h_colidx && A->nnz_v)
-    PSPMM_CUDA_TRY(cudaMemcpy(h_colidx, A->d_colidx, (size_t)A->nnz_v * sizeof(int32_t),
-                              cudaMemcpyDeviceToHost));
-  if (h_val && A->nnz_v)
-    PSPMM_CUDA_TRY(cudaMemcpy(h_val, A->d_val, (size_t)A->nnz_v * A->V * sizeof(float),
-                              cudaMemcpyDeviceToHost));
-  if (h_trow && A->S == 1 && A->num_chunks)
-    PSPMM_CUDA_TRY(cudaMemcpy(h_trow, A->d_trow, (size_t)A->num_chunks * sizeof(int32_t),
-                              cudaMemcpyDeviceToHost));
-  return PSPMM_OK;
+  return pspmm::guarded("pcsr_export", [&]() -> pspmm_status {
+    if (!A) {
+      set_error("pcsr_export: null handle");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    if (h_rowptr)
+      PSPMM_CUDA_TRY(cudaMemcpy(h_rowptr, A->d_rowptr, (size_t)A->rowptr_len * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost));
+    if (h_colidx && A->nnz_v)
+      PSPMM_CUDA_TRY(cudaMemcpy(h_colidx, A->d_colidx, (size_t)A->nnz_v * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost));
+    if (h_val && A->nnz_v)
+      PSPMM_CUDA_TRY(cudaMemcpy(h_val, A->d_val, (size_t)A->nnz_v * A->V * sizeof(float),
+                                cudaMemcpyDeviceToHost));
+    if (h_trow && A->S == 1 && A->num_chunks)
+      PSPMM_CUDA_TRY(cudaMemcpy(h_trow, A->d_trow, (size_t)A->num_chunks * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost));
+    return PSPMM_OK;
+  });
 }
 
 void pspmm_pcsr_destroy(pspmm_pcsr A) {
-  if (!A) return;
+  if (!A) return;  // (nothing below allocates or throws: CUDA frees and delete)
   cudaFree(A->d_rowptr);
   cudaFree(A->d_colidx);
   cudaFree(A->d_val);
@@ -176,206 +200,240 @@ void pspmm_pcsr_destroy(pspmm_pcsr A) {
 
 pspmm_status pspmm_spmm_run(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
                             int64_t ldc, pspmm_config cfg, void *stream) {
-  return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream));
+  return pspmm::guarded("spmm_run", [&]() -> pspmm_status {
+    return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_spmm_accumulate(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
                                    float *d_C, int64_t ldc, pspmm_config cfg, void *stream) {
-  return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream), 1);
+  return pspmm::guarded("spmm_accumulate", [&]() -> pspmm_status {
+    return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream), 1);
+  });
 }
 
 pspmm_status pspmm_spmm_run_fanout(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
                                    float *d_C, int64_t ldc, float *const *h_peers, int32_t npeers,
                                    pspmm_config cfg, void *stream) {
-  if (npeers < 0 || npeers > PSPMM_MAX_PEERS || (npeers > 0 && !h_peers)) {
-    set_error("spmm_run_fanout: npeers must be in 0..PSPMM_MAX_PEERS with a peer array");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  Fanout fan{};
-  fan.n = npeers;
-  for (int d = 0; d < npeers; ++d) fan.peer[d] = h_peers[d];
-  return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream), 0, &fan);
+  return pspmm::guarded("spmm_run_fanout", [&]() -> pspmm_status {
+    if (npeers < 0 || npeers > PSPMM_MAX_PEERS || (npeers > 0 && !h_peers)) {
+      set_error("spmm_run_fanout: npeers must be in 0..PSPMM_MAX_PEERS with a peer array");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    Fanout fan{};
+    fan.n = npeers;
+    for (int d = 0; d < npeers; ++d) fan.peer[d] = h_peers[d];
+    return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream), 0, &fan);
+  });
 }
 
 pspmm_status pspmm_ipc_get_handle(const void *d_ptr, void *h_handle, int64_t *offset) {
-  if (!d_ptr || !h_handle || !offset) {
-    set_error("ipc_get_handle: null argument");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  CUdeviceptr base = 0;
-  size_t size = 0;
-  auto range = get_address_range();
-  if (!range) {
-    set_error("ipc_get_handle: cuMemGetAddressRange unavailable");
-    return PSPMM_ERR_CUDA;
-  }
-  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) {
-    set_error("ipc_get_handle: not a device allocation");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  cudaIpcMemHandle_t h;
-  PSPMM_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
-  memcpy(h_handle, &h, sizeof(h));
-  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
-  return PSPMM_OK;
+  return pspmm::guarded("ipc_get_handle", [&]() -> pspmm_status {
+    if (!d_ptr || !h_handle || !offset) {
+      set_error("ipc_get_handle: null argument");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    auto range = get_address_range();
+    if (!range) {
+      set_error("ipc_get_handle: cuMemGetAddressRange unavailable");
+      return PSPMM_ERR_CUDA;
+    }
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) {
+      set_error("ipc_get_handle: not a device allocation");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    cudaIpcMemHandle_t h;
+    PSPMM_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+    memcpy(h_handle, &h, sizeof(h));
+    *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+    return PSPMM_OK;
+  });
 }
 
 pspmm_status pspmm_ipc_open(const void *h_handle, void **d_base) {
-  if (!h_handle || !d_base) {
-    set_error("ipc_open: null argument");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  cudaIpcMemHandle_t h;
-  memcpy(&h, h_handle, sizeof(h));
-  PSPMM_CUDA_TRY(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
-  return PSPMM_OK;
+  return pspmm::guarded("ipc_open", [&]() -> pspmm_status {
+    if (!h_handle || !d_base) {
+      set_error("ipc_open: null argument");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, h_handle, sizeof(h));
+    PSPMM_CUDA_TRY(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
+    return PSPMM_OK;
+  });
 }
 
 pspmm_status pspmm_ipc_close(void *d_base) {
-  if (!d_base) return PSPMM_OK;
-  PSPMM_CUDA_TRY(cudaIpcCloseMemHandle(d_base));
-  return PSPMM_OK;
+  return pspmm::guarded("ipc_close", [&]() -> pspmm_status {
+    if (!d_base) return PSPMM_OK;
+    PSPMM_CUDA_TRY(cudaIpcCloseMemHandle(d_base));
+    return PSPMM_OK;
+  });
 }
 
 pspmm_status pspmm_spmm_run_host(pspmm_pcsr A, const float *h_B, int64_t ldb, int32_t K,
                                  float *h_C, int64_t ldc, pspmm_config cfg, float *d_Bbuf,
                                  float *d_Cbuf, void *stream) {
-  if (!A || !h_B || !h_C || !d_Bbuf || !d_Cbuf) {
-    set_error("spmm_run_host: null argument");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  if (K < 1 || ldb < K || ldc < K) {
-    set_error("spmm_run_host: need K >= 1, ldb >= K, ldc >= K");
-    return PSPMM_ERR_DIM_MISMATCH;
-  }
-  return run_spmm_host(A, h_B, ldb, K, h_C, ldc, cfg, d_Bbuf, d_Cbuf, as_stream(stream));
+  return pspmm::guarded("spmm_run_host", [&]() -> pspmm_status {
+    if (!A || !h_B || !h_C || !d_Bbuf || !d_Cbuf) {
+      set_error("spmm_run_host: null argument");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    if (K < 1 || ldb < K || ldc < K) {
+      set_error("spmm_run_host: need K >= 1, ldb >= K, ldc >= K");
+      return PSPMM_ERR_DIM_MISMATCH;
+    }
+    return run_spmm_host(A, h_B, ldb, K, h_C, ldc, cfg, d_Bbuf, d_Cbuf, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_spmm_run_host_batch(pspmm_pcsr A, const float *const *h_B, int64_t ldb,
                                        int32_t K, float *const *h_C, int64_t ldc, int32_t count,
                                        pspmm_config cfg, float *const *d_B, float *const *d_C,
                                        void *stream) {
-  if (!A || !h_B || !h_C || !d_B || !d_C || count < 0) {
-    set_error("spmm_run_host_batch: null argument or negative count");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  for (int32_t i = 0; i < count; ++i)
-    if (!h_B[i] || !h_C[i]) {
-      set_error("spmm_run_host_batch: null host matrix");
+  return pspmm::guarded("spmm_run_host_batch", [&]() -> pspmm_status {
+    if (!A || !h_B || !h_C || !d_B || !d_C || count < 0) {
+      set_error("spmm_run_host_batch: null argument or negative count");
       return PSPMM_ERR_INVALID_ARG;
     }
-  for (int b = 0; b < 2; ++b)
-    if (!d_B[b] || !d_C[b]) {
-      set_error("spmm_run_host_batch: null device buffer");
-      return PSPMM_ERR_INVALID_ARG;
+    for (int32_t i = 0; i < count; ++i)
+      if (!h_B[i] || !h_C[i]) {
+        set_error("spmm_run_host_batch: null host matrix");
+        return PSPMM_ERR_INVALID_ARG;
+      }
+    for (int b = 0; b < 2; ++b)
+      if (!d_B[b] || !d_C[b]) {
+        set_error("spmm_run_host_batch: null device buffer");
+        return PSPMM_ERR_INVALID_ARG;
+      }
+    if (K < 1 || ldb < K || ldc < K) {
+      set_error("spmm_run_host_batch: need K >= 1, ldb >= K, ldc >= K");
+      return PSPMM_ERR_DIM_MISMATCH;
     }
-  if (K < 1 || ldb < K || ldc < K) {
-    set_error("spmm_run_host_batch: need K >= 1, ldb >= K, ldc >= K");
-    return PSPMM_ERR_DIM_MISMATCH;
-  }
-  return run_spmm_host_batch(A, h_B, ldb, K, h_C, ldc, count, cfg, d_B, d_C, as_stream(stream));
+    return run_spmm_host_batch(A, h_B, ldb, K, h_C, ldc, count, cfg, d_B, d_C, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_dense_gemm(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
                               const float *d_W, int64_t ldw, float *d_T, int64_t ldt,
                               void *stream) {
-  return dense_gemm(n, Ki, Ko, d_X, ldx, d_W, ldw, d_T, ldt, as_stream(stream));
+  return pspmm::guarded("dense_gemm", [&]() -> pspmm_status {
+    return dense_gemm(n, Ki, Ko, d_X, ldx, d_W, ldw, d_T, ldt, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_gnn_layer(pspmm_pcsr A, const float *d_X, int64_t ldx, int32_t Ki,
                              const float *d_W, int64_t ldw, int32_t Ko, float *d_T, int64_t ldt,
                              float *d_Y, int64_t ldy, pspmm_config cfg, void *stream) {
-  if (!A || !d_X || !d_W || !d_T || !d_Y) {
-    set_error("gnn_layer: null argument");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  if (Ki < 1 || Ko < 1 || ldx < Ki || ldw < Ko || ldy < Ko || ldt < std::min(Ki, Ko)) {
-    set_error("gnn_layer: need Ki, Ko >= 1, ldx >= Ki, ldw >= Ko, ldy >= Ko, ldt >= min(Ki, Ko)");
-    return PSPMM_ERR_DIM_MISMATCH;
-  }
-  cudaStream_t s = as_stream(stream);
-  pspmm_status st;
-  if (Ko <= Ki) {  // T = X . W (n_cols x Ko), Y = A . T: the SpMM runs on Ko columns
-    st = dense_gemm(A->n_cols, Ki, Ko, d_X, ldx, d_W, ldw, d_T, ldt, s);
+  return pspmm::guarded("gnn_layer", [&]() -> pspmm_status {
+    if (!A || !d_X || !d_W || !d_T || !d_Y) {
+      set_error("gnn_layer: null argument");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    if (Ki < 1 || Ko < 1 || ldx < Ki || ldw < Ko || ldy < Ko || ldt < std::min(Ki, Ko)) {
+      set_error("gnn_layer: need Ki, Ko >= 1, ldx >= Ki, ldw >= Ko, ldy >= Ko, ldt >= min(Ki, Ko)");
+      return PSPMM_ERR_DIM_MISMATCH;
+    }
+    cudaStream_t s = as_stream(stream);
+    pspmm_status st;
+    if (Ko <= Ki) {  // T = X . W (n_cols x Ko), Y = A . T: the SpMM runs on Ko columns
+      st = dense_gemm(A->n_cols, Ki, Ko, d_X, ldx, d_W, ldw, d_T, ldt, s);
+      if (st != PSPMM_OK) return st;
+      return run_spmm(A, d_T, ldt, Ko, d_Y, ldy, cfg, s);
+    }
+    // T = A . X (n x Ki), Y = T . W: the SpMM runs on Ki columns
+    st = run_spmm(A, d_X, ldx, Ki, d_T, ldt, cfg, s);
     if (st != PSPMM_OK) return st;
-    return run_spmm(A, d_T, ldt, Ko, d_Y, ldy, cfg, s);
-  }
-  // T = A . X (n x Ki), Y = T . W: the SpMM runs on Ki columns
-  st = run_spmm(A, d_X, ldx, Ki, d_T, ldt, cfg, s);
-  if (st != PSPMM_OK) return st;
-  return dense_gemm(A->n_rows, Ki, Ko, d_T, ldt, d_W, ldw, d_Y, ldy, s);
+    return dense_gemm(A->n_rows, Ki, Ko, d_T, ldt, d_W, ldw, d_Y, ldy, s);
+  });
 }
 
 pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,
                                  const int32_t *d_rowptr, const int32_t *d_colidx,
                                  const float *d_val, int32_t *d_t_rowptr, int32_t *d_t_colidx,
                                  float *d_t_val, void *stream) {
-  return csr_transpose(n_rows, n_cols, nnz, d_rowptr, d_colidx, d_val, d_t_rowptr, d_t_colidx,
-                       d_t_val, as_stream(stream));
+  return pspmm::guarded("csr_transpose", [&]() -> pspmm_status {
+    return csr_transpose(n_rows, n_cols, nnz, d_rowptr, d_colidx, d_val, d_t_rowptr, d_t_colidx,
+                         d_t_val, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_csr_permute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                                const int32_t *d_colidx, const float *d_val, const int32_t *d_perm,
                                int32_t *d_out_rowptr, int32_t *d_out_colidx, float *d_out_val,
                                void *stream) {
-  return csr_permute(n, nnz, d_rowptr, d_colidx, d_val, d_perm, d_out_rowptr, d_out_colidx,
-                     d_out_val, as_stream(stream));
+  return pspmm::guarded("csr_permute", [&]() -> pspmm_status {
+    return csr_permute(n, nnz, d_rowptr, d_colidx, d_val, d_perm, d_out_rowptr, d_out_colidx,
+                       d_out_val, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_permute_rows(int64_t n, int32_t K, const float *d_in, int64_t ldi,
                                 const int32_t *d_perm, float *d_out, int64_t ldo, int32_t inverse,
                                 void *stream) {
-  return permute_rows(n, K, d_in, ldi, d_perm, d_out, ldo, inverse, as_stream(stream));
+  return pspmm::guarded("permute_rows", [&]() -> pspmm_status {
+    return permute_rows(n, K, d_in, ldi, d_perm, d_out, ldo, inverse, as_stream(stream));
+  });
 }
 
 pspmm_status pspmm_features_compute(int64_t n, int64_t nnz, const int32_t *d_rowptr,
                                     const int32_t *d_colidx, int32_t omega, void *stream,
                                     pspmm_features *out) {
-  return compute_features(n, nnz, d_rowptr, d_colidx, omega, as_stream(stream), out);
+  return pspmm::guarded("features_compute", [&]() -> pspmm_status {
+    return compute_features(n, nnz, d_rowptr, d_colidx, omega, as_stream(stream), out);
+  });
 }
 
 pspmm_status pspmm_pcsr_attach_dense(pspmm_pcsr A, const int32_t *d_rowptr,
                                      const int32_t *d_colidx, const float *d_val,
                                      double min_density, int32_t k_max, void *stream,
                                      int64_t *out_tiles) {
-  return attach_dense(A, d_rowptr, d_colidx, d_val, min_density, k_max, as_stream(stream),
-                      out_tiles);
+  return pspmm::guarded("pcsr_attach_dense", [&]() -> pspmm_status {
+    return attach_dense(A, d_rowptr, d_colidx, d_val, min_density, k_max, as_stream(stream),
+                        out_tiles);
+  });
 }
 
 pspmm_status pspmm_decide_dense(pspmm_pcsr A, int32_t K, double min_frac, pspmm_config *cfg) {
-  if (!A || !cfg || K < 1 || !(min_frac >= 0.0 && min_frac <= 1.0)) {
-    set_error("decide_dense: null argument, K < 1 or min_frac outside [0, 1]");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  if (A->dense && A->dense->num_tiles > 0 && K % 16 == 0 && A->nnz > 0 &&
-      (double)A->dense->nnz_dense >= min_frac * (double)A->nnz) {
-    cfg->mode = 1;
-    // the rest is its own sparse matrix: the decider's mode-0 knobs for its
-    // features (a TMA-gather label, mode 2, has no W / F / G for mode 0)
-    pspmm_config rc{};
-    if (A->dense->rest_f_ok && pspmm_decide_config(&A->dense->rest_f, K, &rc) == PSPMM_OK &&
-        rc.mode != 2 && rc.F >= 1) {
-      cfg->W = rc.W;
-      cfg->F = rc.F;
-      cfg->G = rc.G;
-      cfg->order = rc.order;
+  return pspmm::guarded("decide_dense", [&]() -> pspmm_status {
+    if (!A || !cfg || K < 1 || !(min_frac >= 0.0 && min_frac <= 1.0)) {
+      set_error("decide_dense: null argument, K < 1 or min_frac outside [0, 1]");
+      return PSPMM_ERR_INVALID_ARG;
     }
-  } else if (cfg->mode == 1)
-    cfg->mode = 0;
-  return PSPMM_OK;
+    if (A->dense && A->dense->num_tiles > 0 && K % 16 == 0 && K <= A->dense->k_max && A->nnz > 0 &&
+        (double)A->dense->nnz_dense >= min_frac * (double)A->nnz) {
+      cfg->mode = 1;
+      // the rest is its own sparse matrix: the decider's mode-0 knobs for its
+      // features (a TMA-gather label, mode 2, has no W / F / G for mode 0)
+      pspmm_config rc{};
+      if (A->dense->rest_f_ok && pspmm_decide_config(&A->dense->rest_f, K, &rc) == PSPMM_OK &&
+          rc.mode != 2 && rc.F >= 1) {
+        cfg->W = rc.W;
+        cfg->F = rc.F;
+        cfg->G = rc.G;
+        cfg->order = rc.order;
+      }
+    } else if (cfg->mode == 1)
+      cfg->mode = 0;
+    return PSPMM_OK;
+  });
 }
 
 pspmm_status pspmm_pcsr_dense_info(pspmm_pcsr A, int64_t *num_panels, int64_t *num_tiles,
                                    int64_t *nnz_dense) {
-  if (!A || !num_panels || !num_tiles || !nnz_dense) {
-    set_error("pcsr_dense_info: null argument");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  *num_panels = A->dense ? A->dense->num_panels : 0;
-  *num_tiles = A->dense ? A->dense->num_tiles : 0;
-  *nnz_dense = A->dense ? A->dense->nnz_dense : 0;
-  return PSPMM_OK;
+  return pspmm::guarded("pcsr_dense_info", [&]() -> pspmm_status {
+    if (!A || !num_panels || !num_tiles || !nnz_dense) {
+      set_error("pcsr_dense_info: null argument");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    *num_panels = A->dense ? A->dense->num_panels : 0;
+    *num_tiles = A->dense ? A->dense->num_tiles : 0;
+    *nnz_dense = A->dense ? A->dense->nnz_dense : 0;
+    return PSPMM_OK;
+  });
 }
 
 }  // extern "C"

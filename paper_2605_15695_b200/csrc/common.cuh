@@ -6,6 +6,7 @@
 
 #include <string>
 
+#include "guard.h"
 #include "pspmm.h"
 
 // The PCSR handle: rowPtr / colIdx / val / TRow on the device, plus

@@ -8,6 +8,7 @@
 //   S = 1 iff d_max > 8 d^     (balancing pays on skewed degrees)
 //   F: smallest coarsening whose row group fits in a warp with no MAC-job gap
 //      (Eq. 1 generalised to 4G lanes).
+#include "guard.h"
 #include <cmath>
 
 #include "decider_model.h"
@@ -61,78 +62,80 @@ double feature_value(const pspmm_features *f, int idx, int K) {
 
 extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
                                             pspmm_config *out) {
-  if (!f || !out || K < 1) return PSPMM_ERR_INVALID_ARG;
-  if (!(f->nnz > 0)) return PSPMM_ERR_EMPTY;
-  pspmm_config c{};
-  c.omega = 32;
-  c.sg_override = 0;
-  c.mode = 0;
-#if PSPMM_DECIDER_TRAINED
-  // random forest: every tree votes for its leaf's label; the label
-  // with the most votes wins, ties to the lowest label id
-  int votes[pspmm_model::kNumLabels] = {};
-  for (int t = 0; t < pspmm_model::kTrees; ++t) {
-    int node = pspmm_model::kRoot[t];
-    while (pspmm_model::kFeature[node] >= 0) {
-      const double x = feature_value(f, pspmm_model::kFeature[node], K);
-      node = x <= pspmm_model::kThreshold[node] ? pspmm_model::kLeft[node]
-                                                : pspmm_model::kRight[node];
+  return pspmm::guarded("decide_config", [&]() -> pspmm_status {
+    if (!f || !out || K < 1) return PSPMM_ERR_INVALID_ARG;
+    if (!(f->nnz > 0)) return PSPMM_ERR_EMPTY;
+    pspmm_config c{};
+    c.omega = 32;
+    c.sg_override = 0;
+    c.mode = 0;
+  #if PSPMM_DECIDER_TRAINED
+    // random forest: every tree votes for its leaf's label; the label
+    // with the most votes wins, ties to the lowest label id
+    int votes[pspmm_model::kNumLabels] = {};
+    for (int t = 0; t < pspmm_model::kTrees; ++t) {
+      int node = pspmm_model::kRoot[t];
+      while (pspmm_model::kFeature[node] >= 0) {
+        const double x = feature_value(f, pspmm_model::kFeature[node], K);
+        node = x <= pspmm_model::kThreshold[node] ? pspmm_model::kLeft[node]
+                                                  : pspmm_model::kRight[node];
+      }
+      votes[pspmm_model::kLeafLabel[node]]++;
     }
-    votes[pspmm_model::kLeafLabel[node]]++;
-  }
-  int best = 0;
-  for (int l = 1; l < pspmm_model::kNumLabels; ++l)
-    if (votes[l] > votes[best]) best = l;
-  const int *lab = pspmm_model::kLabel[best];
-  c.mode = lab[0];
-  c.V = lab[1];
-  c.S = lab[2];
-  c.W = lab[3];
-  c.order = c.mode == 0 ? lab[6] : 0;
-  if (c.mode == 2 && K % 32 != 0) c.mode = 0;  // TMA engine needs K % 32 == 0
-  if ((c.mode == 3 || c.mode == 4) && K % 4 != 0) c.mode = 0;  // short-row engines: 128-bit only
-  // the short-row engines walk a row's vectors beyond the staged window one
-  // dependent load at a time: a hub row serialises its group (K sweep,
-  // Cora K = 128, mode 3 0.059 ms vs cuSPARSE 0.023), so
-  // graphs with rows longer than 64 vectors stay on mode 0
-  if ((c.mode == 3 || c.mode == 4) && f->d_max > 64.0) c.mode = 0;
-  // vectorized blocking only where it saves B reads: at PR_2 ~ 0.5 a V = 2
-  // vector is a padded single value (the paper's T1: V = 2 loses
-  // at PR 47.8-49 %); the forest's V = 2 there extrapolates a noise-level
-  // label (products K = 128) to other graphs (Reddit K = 128: 4.46 ms with
-  // V = 2 vs 3.22 ms with V = 1)
-  if (c.V == 2 && f->pr2 >= 0.45) c.V = 1;
-  if (c.mode == 2) {
-    pick_fg(K, 0, &c.F, &c.G);  // unused by mode 2; a valid mode-0 fallback
-  } else if (lab[0] == 2) {
+    int best = 0;
+    for (int l = 1; l < pspmm_model::kNumLabels; ++l)
+      if (votes[l] > votes[best]) best = l;
+    const int *lab = pspmm_model::kLabel[best];
+    c.mode = lab[0];
+    c.V = lab[1];
+    c.S = lab[2];
+    c.W = lab[3];
+    c.order = c.mode == 0 ? lab[6] : 0;
+    if (c.mode == 2 && K % 32 != 0) c.mode = 0;  // TMA engine needs K % 32 == 0
+    if ((c.mode == 3 || c.mode == 4) && K % 4 != 0) c.mode = 0;  // short-row engines: 128-bit only
+    // the short-row engines walk a row's vectors beyond the staged window one
+    // dependent load at a time: a hub row serialises its group (K sweep,
+    // Cora K = 128, mode 3 0.059 ms vs cuSPARSE 0.023), so
+    // graphs with rows longer than 64 vectors stay on mode 0
+    if ((c.mode == 3 || c.mode == 4) && f->d_max > 64.0) c.mode = 0;
+    // vectorized blocking only where it saves B reads: at PR_2 ~ 0.5 a V = 2
+    // vector is a padded single value (the paper's T1: V = 2 loses
+    // at PR 47.8-49 %); the forest's V = 2 there extrapolates a noise-level
+    // label (products K = 128) to other graphs (Reddit K = 128: 4.46 ms with
+    // V = 2 vs 3.22 ms with V = 1)
+    if (c.V == 2 && f->pr2 >= 0.45) c.V = 1;
+    if (c.mode == 2) {
+      pick_fg(K, 0, &c.F, &c.G);  // unused by mode 2; a valid mode-0 fallback
+    } else if (lab[0] == 2) {
+      pick_fg(K, 0, &c.F, &c.G);
+    } else {
+      // G from the label's column-pass count P: the smallest power of two with
+      // 4 G F P >= K (capped at 32 lanes)
+      c.F = lab[4];
+      const int P = lab[5];
+      const int q = (K + 3) / 4;
+      c.G = ceil_pow2((q + c.F * P - 1) / (c.F * P));
+      // B far beyond L2 (the training corpus has no such graph at large K):
+      // every column pass re-gathers one B segment per nonzero, and the
+      // gather cost is per segment, so take one pass of 32 lanes (K sweep,
+      // products K = 256, 4 passes 27.8 ms vs cuSPARSE 23.4)
+      const int passes = (K + 4 * c.G * c.F - 1) / (4 * c.G * c.F);
+      if (c.mode == 0 && passes > 1 && f->n * (double)K * 4.0 > 2.0 * kL2Bytes &&
+          (q + 31) / 32 <= 8) {
+        c.F = (q + 31) / 32;
+        c.G = ceil_pow2((q + c.F - 1) / c.F);
+      }
+    }
+    *out = c;
+    return PSPMM_OK;
+  #else
+    (void)feature_value;
+    c.V = f->pr2 < 0.30 ? 2 : 1;
+    c.S = f->d_max > 8.0 * f->d_hat ? 1 : 0;
+    c.W = 4;
     pick_fg(K, 0, &c.F, &c.G);
-  } else {
-    // G from the label's column-pass count P: the smallest power of two with
-    // 4 G F P >= K (capped at 32 lanes)
-    c.F = lab[4];
-    const int P = lab[5];
-    const int q = (K + 3) / 4;
-    c.G = ceil_pow2((q + c.F * P - 1) / (c.F * P));
-    // B far beyond L2 (the training corpus has no such graph at large K):
-    // every column pass re-gathers one B segment per nonzero, and the
-    // gather cost is per segment, so take one pass of 32 lanes (K sweep,
-    // products K = 256, 4 passes 27.8 ms vs cuSPARSE 23.4)
-    const int passes = (K + 4 * c.G * c.F - 1) / (4 * c.G * c.F);
-    if (c.mode == 0 && passes > 1 && f->n * (double)K * 4.0 > 2.0 * kL2Bytes &&
-        (q + 31) / 32 <= 8) {
-      c.F = (q + 31) / 32;
-      c.G = ceil_pow2((q + c.F - 1) / c.F);
-    }
-  }
-  *out = c;
-  return PSPMM_OK;
-#else
-  (void)feature_value;
-  c.V = f->pr2 < 0.30 ? 2 : 1;
-  c.S = f->d_max > 8.0 * f->d_hat ? 1 : 0;
-  c.W = 4;
-  pick_fg(K, 0, &c.F, &c.G);
-  *out = c;
-  return PSPMM_OK;
-#endif
+    *out = c;
+    return PSPMM_OK;
+  #endif
+  });
 }

@@ -12,6 +12,7 @@
 //               hub rows of B that most nonzeros gather together
 //
 // perm[old] = new.  The graph is treated as undirected (A + A^T pattern).
+#include "guard.h"
 #include <algorithm>
 #include <numeric>
 #include <string>
@@ -103,61 +104,63 @@ void bfs(const Graph &g, int32_t s, std::vector<int32_t> &stamp, int32_t tag,
 
 extern "C" pspmm_status pspmm_reorder(int64_t n, const int32_t *h_rowptr, const int32_t *h_colidx,
                                       int32_t strategy, int32_t *h_perm) {
-  if (n < 1 || !h_rowptr || !h_perm || (h_rowptr[n] > 0 && !h_colidx)) {
-    pspmm::set_error("reorder: bad arguments");
-    return PSPMM_ERR_INVALID_ARG;
-  }
-  if (strategy == 0) {
-    for (int64_t i = 0; i < n; ++i) h_perm[i] = (int32_t)i;
-    return PSPMM_OK;
-  }
-  Graph g = symmetrize(n, h_rowptr, h_colidx);
-  auto degree = [&](int64_t v) { return g.ptr[v + 1] - g.ptr[v]; };
-  if (strategy == 2) {
-    std::vector<int32_t> idx(n);
-    std::iota(idx.begin(), idx.end(), 0);
-    std::stable_sort(idx.begin(), idx.end(),
-                     [&](int32_t a, int32_t b) { return degree(a) > degree(b); });
-    for (int64_t k = 0; k < n; ++k) h_perm[idx[k]] = (int32_t)k;
-    return PSPMM_OK;
-  }
-  if (strategy != 1) {
-    pspmm::set_error("reorder: strategy must be 0 (identity), 1 (BFS) or 2 (degree)");
-    return PSPMM_ERR_CONFIG;
-  }
-  // components (in node order), then numbered in descending size
-  std::vector<int32_t> stamp(n, -1), order, comp_of(n, -1);
-  std::vector<std::pair<int64_t, int32_t>> comps;  // (size, representative)
-  int32_t tag = 0;
-  for (int64_t v = 0; v < n; ++v) {
-    if (stamp[v] >= 0) continue;
-    bfs(g, (int32_t)v, stamp, tag, order, nullptr, false);
-    // lowest-degree node of the component starts the peripheral search
-    int32_t best = order[0];
-    for (int32_t u : order)
-      if (degree(u) < degree(best)) best = u;
-    comps.push_back({(int64_t)order.size(), best});
-    ++tag;
-  }
-  std::stable_sort(comps.begin(), comps.end(),
-                   [](const auto &a, const auto &b) { return a.first > b.first; });
-  std::vector<int32_t> level(n, 0);
-  std::vector<int32_t> stamp2(n, -1);
-  int64_t next = 0;
-  int32_t tag2 = 0;
-  for (const auto &c : comps) {
-    // George-Liu: two sweeps toward a pseudo-peripheral node
-    int32_t s = c.second;
-    for (int sweep = 0; sweep < 2; ++sweep) {
-      bfs(g, s, stamp2, tag2++, order, &level, false);
-      const int32_t far_level = level[order.back()];
-      int32_t cand = order.back();
-      for (int32_t u : order)
-        if (level[u] == far_level && degree(u) < degree(cand)) cand = u;
-      s = cand;
+  return pspmm::guarded("reorder", [&]() -> pspmm_status {
+    if (n < 1 || !h_rowptr || !h_perm || (h_rowptr[n] > 0 && !h_colidx)) {
+      pspmm::set_error("reorder: bad arguments");
+      return PSPMM_ERR_INVALID_ARG;
     }
-    bfs(g, s, stamp2, tag2++, order, nullptr, true);
-    for (int32_t u : order) h_perm[u] = (int32_t)(next++);
-  }
-  return PSPMM_OK;
+    if (strategy == 0) {
+      for (int64_t i = 0; i < n; ++i) h_perm[i] = (int32_t)i;
+      return PSPMM_OK;
+    }
+    Graph g = symmetrize(n, h_rowptr, h_colidx);
+    auto degree = [&](int64_t v) { return g.ptr[v + 1] - g.ptr[v]; };
+    if (strategy == 2) {
+      std::vector<int32_t> idx(n);
+      std::iota(idx.begin(), idx.end(), 0);
+      std::stable_sort(idx.begin(), idx.end(),
+                       [&](int32_t a, int32_t b) { return degree(a) > degree(b); });
+      for (int64_t k = 0; k < n; ++k) h_perm[idx[k]] = (int32_t)k;
+      return PSPMM_OK;
+    }
+    if (strategy != 1) {
+      pspmm::set_error("reorder: strategy must be 0 (identity), 1 (BFS) or 2 (degree)");
+      return PSPMM_ERR_CONFIG;
+    }
+    // components (in node order), then numbered in descending size
+    std::vector<int32_t> stamp(n, -1), order, comp_of(n, -1);
+    std::vector<std::pair<int64_t, int32_t>> comps;  // (size, representative)
+    int32_t tag = 0;
+    for (int64_t v = 0; v < n; ++v) {
+      if (stamp[v] >= 0) continue;
+      bfs(g, (int32_t)v, stamp, tag, order, nullptr, false);
+      // lowest-degree node of the component starts the peripheral search
+      int32_t best = order[0];
+      for (int32_t u : order)
+        if (degree(u) < degree(best)) best = u;
+      comps.push_back({(int64_t)order.size(), best});
+      ++tag;
+    }
+    std::stable_sort(comps.begin(), comps.end(),
+                     [](const auto &a, const auto &b) { return a.first > b.first; });
+    std::vector<int32_t> level(n, 0);
+    std::vector<int32_t> stamp2(n, -1);
+    int64_t next = 0;
+    int32_t tag2 = 0;
+    for (const auto &c : comps) {
+      // George-Liu: two sweeps toward a pseudo-peripheral node
+      int32_t s = c.second;
+      for (int sweep = 0; sweep < 2; ++sweep) {
+        bfs(g, s, stamp2, tag2++, order, &level, false);
+        const int32_t far_level = level[order.back()];
+        int32_t cand = order.back();
+        for (int32_t u : order)
+          if (level[u] == far_level && degree(u) < degree(cand)) cand = u;
+        s = cand;
+      }
+      bfs(g, s, stamp2, tag2++, order, nullptr, true);
+      for (int32_t u : order) h_perm[u] = (int32_t)(next++);
+    }
+    return PSPMM_OK;
+  });
 }

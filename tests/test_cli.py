@@ -82,3 +82,13 @@ def test_bench_lattice_covers_dim(dim):
         assert V in (1, 2) and S in (0, 1) and W in (2, 4, 8)
         assert G & (G - 1) == 0 and G <= 32
         assert G * F >= q or G == 32
+
+
+def test_mtx_explicit_zeros_dropped(tmp_path):
+    """SPEC load_matrix_market: explicit zeros (and duplicates summing to 0)
+    are not stored, so nnz and the Table-3 features see only true nonzeros."""
+    p = _write(tmp_path, "%%MatrixMarket matrix coordinate real general\n"
+               "3 3 5\n1 1 0.0\n1 2 2.0\n2 3 1.5\n2 3 -1.5\n3 1 4\n")
+    rp, ci, val, n, nc = cli.read_mtx(p)
+    assert rp.tolist() == [0, 1, 1, 2]
+    assert ci.tolist() == [1, 0] and val.tolist() == [2.0, 4.0]
