@@ -154,13 +154,16 @@ def gather_roofline(name, head, K, ms):
             "ceiling_tbps": ceil["tbps"], "frac": tbps / ceil["tbps"], "source": ceil["source"]}
 
 
-def traffic_for(name, cfg):
+def traffic_for(name, cfg, cfg_dict=None):
+    """ncu DRAM bytes per launch of the decided config (profiles/traffic.json),
+    or None when the committed capture is of another config."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             t = json.load(f)
         e = t.get(name)
-        if e and all(e["cfg"].get(k) == v for k, v in cfg.as_dict().items() if k in e["cfg"]):
+        cd = cfg_dict if cfg_dict is not None else cfg.as_dict()
+        if e and all(e["cfg"].get(k) == v for k, v in cd.items() if k in e["cfg"]):
             return e["dram_bytes_per_launch"]
     except Exception:
         pass
@@ -247,7 +250,7 @@ def cpu_oracle_sample(g, B, target_s=12.0, threads=None):
     def run(rows):
         t0 = time.perf_counter()
         oracle.spmm(g.rowptr, g.colidx, g.val, B, rows=np.arange(rows, dtype=np.int64),
-                    threads=threads)
+                    threads=threads, with_mag=False)
         return time.perf_counter() - t0
 
     # pilot on ~0.5% of the nonzeros, then scale to the target duration
@@ -263,7 +266,8 @@ def cpu_oracle_sample(g, B, target_s=12.0, threads=None):
     return {"value": 2.0 * nnz_s * K / t / 1e9, "unit": "GFLOP/s", "cores": int(threads),
             "kind": "oracle",
             "sample": f"rows [0, {rows}) of {g.n} ({nnz_s} of {g.nnz} nnz, K={K}), "
-                      f"{t:.1f} s wall, fp64 C = A.B without the |a||b| bound",
+                      f"{t:.1f} s wall, fp64 C = A.B only (oracle.spmm with_mag=False: the "
+                      f"tolerance bound sum |a||b| is not computed)",
             "seconds": t}
 
 
@@ -286,16 +290,21 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
                              stream)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
+    A_dec, cfg0 = A, cfg
     # engine mode 1 (dense 128 x 32 tiles on tcgen05 + the rest): split once
     # per graph, taken when the tiles hold enough of A
     cfg, dense = api.auto_dense(A, rp, ci, vl, K, cfg, stream)
     if dense is not None:
         dense["dense_frac"] = dense["nnz_dense"] / max(1, g.nnz)
+    # engine mode 5 (row blocks, B windows staged in shared memory): taken
+    # when each staged B row would serve enough nonzeros (device-measured)
+    cfg, A, blocks = api.auto_blocks(A, rp, ci, vl, K, cfg, stream)
     t3 = time.perf_counter()
     B = gen.config_B(g.name, g.n)
     Bd = torch.from_numpy(B).cuda()
     C = torch.empty((g.n, K), device="cuda")
-    launches_per_step = 1 + (1 if (A.info["S"] == 1 and A.info["num_chunks"] > A.info["num_panels"])
+    launches_per_step = 1 + (1 if (A.info["S"] == 1 and A.info["num_chunks"] > A.info["num_panels"]
+                                   and cfg.mode != 5)
                              else 0) + (2 if cfg.mode == 1 else 0)  # mode 1: + split_b, dense_tc
 
     def step():
@@ -303,12 +312,17 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
 
     ts = time_steps(step, steps, warmup, flush, stream, sampler)
     ms = float(np.mean(ts))
+    # SURVEY §8(d)'s primary leg: warm back-to-back launches (no flush; the
+    # steady state of an iterative GNN), median, beside the cold mean above
+    tw = time_steps(step, max(steps, 20), 2, lambda: None, stream)
     mode0 = None
-    if cfg.mode == 1:  # the same knobs on the mode-0 engine alone, for comparison
-        c0 = api.Config(**cfg.as_dict())
+    if cfg.mode in (1, 5):  # the decider's mode-0 pick alone, for comparison
+        c0 = api.Config(**(cfg.as_dict() if cfg.mode == 1 else cfg0.as_dict()))
         c0.mode = 0
-        t0s = time_steps(lambda: A.run(Bd, C, c0, stream), steps, warmup, flush, stream)
-        mode0 = {"cfg": c0.as_dict(), "ms_median": float(np.median(t0s))}
+        A0 = A if cfg.mode == 1 else A_dec
+        t0s = time_steps(lambda: A0.run(Bd, C, c0, stream), steps, warmup, flush, stream)
+        mode0 = {"cfg": c0.as_dict(), "ms_median": float(np.median(t0s)),
+                 "ms_mean": float(np.mean(t0s))}
     R = algorithmic_bytes(g.n, g.n, g.nnz, K)
     flops = 2.0 * g.nnz * K
     out = {
@@ -316,6 +330,7 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
         "cfg": cfg.as_dict(), "features": feats, "pcsr": {k: A.info[k] for k in
                                                            ("nnz_v", "num_chunks", "sg", "pr", "sr")},
         "ms_mean": ms, "ms_median": float(np.median(ts)), "ms_min": float(min(ts)),
+        "warm_ms_median": float(np.median(tw)), "warm_ms_min": float(min(tw)),
         "gflops": flops / (ms * 1e-3) / 1e9, "algorithmic_bytes": R,
         "achieved_gbs": R / (ms * 1e-3) / 1e9, "launches_per_step": launches_per_step,
         "preprocess_s": {"features_decide": t1 - t0, "pcsr_build": t2 - t1,
@@ -323,6 +338,8 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
     }
     if dense is not None:
         out["dense_split"] = dense
+    if blocks is not None:
+        out["row_blocks"] = blocks
     if mode0 is not None:
         out["mode0_same_knobs"] = mode0
     if want_cusparse:
@@ -376,7 +393,7 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
                             "dense_gemm_gbs": 8.0 * g.n * K / (mg * 1e-3) / 1e9,
                             "what": f"pspmm_gnn_layer: Y = A (X W), W {K}x{K}; flops 2 nnz K + "
                                     "2 n K^2; dense_gemm_gbs = X read + T written"}
-    del A, rp, ci, vl, Bd, C
+    del A, A_dec, rp, ci, vl, Bd, C
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     return out
@@ -409,6 +426,24 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        # never time fewer ranks than asked: re-launch under torchrun when the
+        # GPUs are there, else fail loudly
+        if "WORLD_SIZE" in os.environ or args.gpus < 1:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} requested but only {have} GPU(s) are "
+                     f"visible; refusing to time fewer ranks than asked")
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                  "--master-port", str(port), os.path.abspath(__file__)]
+                 + sys.argv[1:])
 
     if args.impl == "reference":
         return run_reference(args, world, rank)
@@ -452,7 +487,9 @@ def main():
 
     achieved = R / (roof_ms * 1e-3) / 1e9
     from paper_2605_15695_b200 import api
-    traffic = traffic_for(args.workload, api.Config(**cfg_d))
+    # ncu DRAM traffic exists only for the single-GPU launch (ncu never wraps a
+    # multi-rank command); a shard's traffic is not the 1-GPU figure
+    traffic = traffic_for(args.workload, api.Config(**cfg_d)) if world == 1 else None
     line = {
         "metric": "SpMM GFLOP/s (2*nnz*K/t)",
         "value": value,
@@ -506,15 +543,43 @@ def main():
                     r = measure_single(gg, args.steps, args.warmup, flush, stream,
                                        want_cusparse=not args.no_cusparse, want_e2e=False)
                 r["roofline_frac"] = r["achieved_gbs"] / peak
+                r["name"] = name
                 # realised Table-3 features of every workload stay in the line
                 per.append(r)
                 del gg
             line["per_config"] = per
+    # last key of the line (the driver keeps the line's tail): one compact
+    # row per workload — engine config, cold mean / warm median ms, R-roofline
+    # fraction, DRAM traffic over R (ncu, profiles/traffic.json), cuSPARSE
+    if rank == 0:
+        rows = [dict(head, name=args.workload)] if world == 1 else []
+        rows += [dict(r, name=r.get("name", "")) for r in line.get("per_config", [])]
+        line["summary"] = [summary_row(r, peak) for r in rows]
+        if world > 1:
+            line["summary"] = {"exchange_legs": head.get("exchange_legs")}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def cfg_str(c):
+    return (f"m{c['mode']} V{c['V']} S{c['S']} W{c['W']} F{c['F']} G{c['G']}"
+            + (f" o{c['order']}" if c.get("order") else ""))
+
+
+def summary_row(r, peak):
+    """One compact record of a measured workload (bench line summary)."""
+    R = r["algorithmic_bytes"]
+    tr = traffic_for(r["name"], None, r["cfg"])
+    out = {"w": r["name"], "K": r["K"], "cfg": cfg_str(r["cfg"]), "ms": round(r["ms_mean"], 4),
+           "warm_ms": round(r.get("warm_ms_median", float("nan")), 4),
+           "frac": round(R / (r["ms_mean"] * 1e-3) / 1e9 / peak, 4),
+           "dram_over_R": round(tr / R, 2) if tr else None}
+    if r.get("speedup_vs_cusparse_best"):
+        out["vs_cusparse"] = round(r["speedup_vs_cusparse_best"], 2)
+    return out
 
 
 def max_over_ranks(vals):
@@ -529,17 +594,20 @@ def max_over_ranks(vals):
 
 def run_sharded(g, args, world, rank, stream, flush, sampler):
     """N > 1: this rank's row shard of the fixed graph (strong scaling).  Step =
-    exchange of B rows + local SpMM.  Exchange: NCCL all-gather overlapped with
-    the own-column block (default for dense halos such as the shuffled
-    Reddit-shaped graph), or a halo all_to_all of only the referenced rows
-    (locality-ordered graphs), or (f2 i) no collective at all: the SpMM epilogue
-    stores every output row into every rank's next-layer B over CUDA-IPC peer
-    memory (FanoutSpmm), followed by a one-element all-reduce barrier.
-    --exchange auto: halo by halo volume, else fanout when the peers map and
-    one validated step matches the plain engine, else the overlapped
-    all-gather."""
+    exchange of B rows + local SpMM.  Every applicable exchange is timed as its
+    own leg (`exchange_legs` in the line), each with its per-rank max step and
+    kernel time and the bytes it moves per rank:
+      allgather  NCCL all-gather of B overlapped with the own-column block
+                 (the north star's row e; headline for dense halos such as the
+                 shuffled Reddit-shaped graph)
+      fanout     (f2 i) no collective: the SpMM epilogue stores every output
+                 row into every rank's next-layer B over CUDA-IPC peer memory,
+                 then a one-element all-reduce barrier
+      halo       (f2 ii) all_to_all of only the referenced rows (headline for
+                 locality-ordered graphs, where < 50 % of the remote rows are
+                 referenced)
+    --exchange X makes X the headline leg (and times only X)."""
     import torch
-    import torch.distributed as dist
     from paper_2605_15695_b200 import api, dist as pdist
     K = g.K
     rp = torch.from_numpy(g.rowptr).cuda()
@@ -550,112 +618,132 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
     B = gen.config_B(g.name, g.n)
     bounds = api.pspmm_shard_plan(g.rowptr, world, 2)
     (frac,) = max_over_ranks([pdist.halo_fraction(g.rowptr, g.colidx, bounds, rank)])
-    use_halo = args.exchange == "halo" or (args.exchange == "auto" and frac < 0.5)
-    fanout, fanout_note = None, None
-    # (gloo: the single-GPU rehearsal of the flow, --exchange fanout only)
-    if not use_halo and (args.exchange == "fanout" or
-                         (args.exchange == "auto" and args.dist_backend == "nccl")):
-        fanout, fanout_note = setup_fanout(g, cfg, gen.config_B(g.name, g.n), world, rank,
-                                           stream)
+    if args.exchange != "auto":
+        legs = [args.exchange]
+    elif frac < 0.5:
+        legs = ["halo", "allgather"]
+    else:
+        legs = ["allgather", "fanout"]
 
     def launches(h):  # engine kernel + the split-panel zeroing kernel when present
         return 1 + (1 if (h.info["S"] == 1 and h.info["num_chunks"] > h.info["num_panels"])
                     else 0)
 
-    if fanout is not None:
-        run = fanout
-        sh = run.shard
-        lo, rows = sh.lo, sh.rows
-        n_cols, nnz_loc = sh.n_cols, int(sh.rowptr[-1])
-        split = run.A.info["S"] == 1 and run.A.info["num_chunks"] > run.A.info["num_panels"]
-        A_launch = 1 + (world if split else 0)  # engine + split-row zeroing per copy
-        C_k = torch.empty((rows, K), device="cuda")
-        dB = torch.zeros((sh.n_max, K), device="cuda")
+    def setup(kind):
+        """-> dict(step, kernel_only, e2e_body, lo, rows, n_cols, nnz_loc, launches,
+        desc, moved) or a string saying why the leg is unavailable."""
+        if kind == "fanout":
+            run, note = setup_fanout(g, cfg, B, world, rank, stream)
+            if run is None:
+                return note or "fanout unavailable"
+            sh = run.shard
+            split = run.A.info["S"] == 1 and run.A.info["num_chunks"] > run.A.info["num_panels"]
+            C_k = torch.empty((sh.rows, K), device="cuda")
+            dB = torch.zeros((sh.n_max, K), device="cuda")
 
-        def step():  # one layer: SpMM whose epilogue stores every row at every rank
-            run.step(stream, swap=False)
+            def e2e_body(hB, hC):
+                dB[:sh.rows].copy_(hB, non_blocking=True)
+                pdist.all_gather_rows(dB, run.X[0])
+                run.step(stream, swap=False)
+                hC.copy_(run.own(1), non_blocking=True)
+            return dict(
+                step=lambda: run.step(stream, swap=False),
+                kernel_only=lambda: run.A.run(run.X[0], C_k, cfg, stream),
+                e2e_body=e2e_body, lo=sh.lo, rows=sh.rows, n_cols=sh.n_cols,
+                nnz_loc=int(sh.rowptr[-1]), launches=1 + (world if split else 0),
+                moved=(world - 1) * sh.rows * K * 4, keep=run,
+                desc="pspmm_spmm_run_fanout: SpMM whose epilogue stores each output row into "
+                     "every rank's next-layer B (CUDA-IPC peer memory over NVLink), then a "
+                     "one-element NCCL all-reduce as the layer barrier; no separate collective")
+        if kind == "halo":
+            plan = pdist.make_halo_plan(g.rowptr, g.colidx, g.val, world, rank)
+            with torch.cuda.stream(stream):
+                run = pdist.HaloSpmm(plan, K, cfg, stream=stream)
+            lo, rows = int(plan.bounds[rank]), plan.rows
+            run.B_local.copy_(torch.from_numpy(B[lo:lo + rows]))
 
-        def kernel_only():
-            run.A.run(run.X[0], C_k, cfg, stream)
-
-        def e2e_body(hB, hC):
-            dB[:rows].copy_(hB, non_blocking=True)
-            pdist.all_gather_rows(dB, run.X[0])
-            run.step(stream, swap=False)
-            hC.copy_(run.own(1), non_blocking=True)
-        desc = ("pspmm_spmm_run_fanout: SpMM whose epilogue stores each output row into "
-                "every rank's next-layer B (CUDA-IPC peer memory over NVLink), then a "
-                "one-element NCCL all-reduce as the layer barrier; no separate collective")
-    elif use_halo:
-        plan = pdist.make_halo_plan(g.rowptr, g.colidx, g.val, world, rank)
-        with torch.cuda.stream(stream):
-            run = pdist.HaloSpmm(plan, K, cfg, stream=stream)
-        lo, rows = int(plan.bounds[rank]), plan.rows
-        run.B_local.copy_(torch.from_numpy(B[lo:lo + rows]))
-        n_cols, nnz_loc = rows + plan.n_halo, int(plan.rowptr[-1])
-        A_launch = launches(run.A) + (1 if len(plan.send_idx) else 0)  # + the pack kernel
-
-        def step():
-            run.step(stream)
-
-        def kernel_only():
-            run.A.run(run.B_ext, run.C, cfg, stream)
-
-        def e2e_body(hB, hC):
-            run.B_local.copy_(hB, non_blocking=True)
-            run.step(stream)
-            hC.copy_(run.C, non_blocking=True)
-        desc = "halo all_to_all_single of the referenced B rows (row-gather pack) + SpMM"
-    else:
+            def e2e_body(hB, hC):
+                run.B_local.copy_(hB, non_blocking=True)
+                run.step(stream)
+                hC.copy_(run.C, non_blocking=True)
+            return dict(
+                step=lambda: run.step(stream),
+                kernel_only=lambda: run.A.run(run.B_ext, run.C, cfg, stream),
+                e2e_body=e2e_body, lo=lo, rows=rows, n_cols=rows + plan.n_halo,
+                nnz_loc=int(plan.rowptr[-1]),
+                launches=launches(run.A) + (1 if len(plan.send_idx) else 0),
+                moved=int(plan.n_halo) * K * 4, keep=run,
+                desc="halo all_to_all_single of the referenced B rows (row-gather pack) + SpMM")
         sh = pdist.make_shard(g.rowptr, g.colidx, g.val, world, rank, align=2)
         with torch.cuda.stream(stream):
             run = pdist.ShardedSpmm(sh, K, cfg, stream=stream)
-        lo, rows = sh.lo, sh.rows
-        B_loc = pdist.pad_rows(torch.from_numpy(B[lo:lo + rows]).cuda(), sh.n_max)
-        n_cols, nnz_loc = sh.n_cols, int(sh.rowptr[-1])
+        B_loc = pdist.pad_rows(torch.from_numpy(B[sh.lo:sh.lo + sh.rows]).cuda(), sh.n_max)
         overlap = not args.no_overlap and run.A_own is not None and args.dist_backend == "nccl"
-        A_launch = (launches(run.A_own) + (1 if run.A_rem is not None else 0)) if overlap \
-            else launches(run.A)
         dB = torch.zeros((sh.n_max, K), device="cuda")
 
-        def step():
-            run.step_overlap(B_loc, stream) if overlap else run.step(B_loc, stream)
-
-        def kernel_only():
-            run.A.run(run.B_full, run.C, cfg, stream)
-
         def e2e_body(hB, hC):
-            dB[:rows].copy_(hB, non_blocking=True)
+            dB[:sh.rows].copy_(hB, non_blocking=True)
             run.step_overlap(dB, stream) if overlap else run.step(dB, stream)
-            hC.copy_(run.C[:rows], non_blocking=True)
-        desc = ("async all_gather_into_tensor(B) || own-column block SpMM, then remote-column "
-                "block pspmm_spmm_accumulate" if overlap else
-                "all_gather_into_tensor(B) then pspmm_spmm_run on the local shard")
+            hC.copy_(run.C[:sh.rows], non_blocking=True)
+        return dict(
+            step=(lambda: run.step_overlap(B_loc, stream)) if overlap else
+                 (lambda: run.step(B_loc, stream)),
+            kernel_only=lambda: run.A.run(run.B_full, run.C, cfg, stream),
+            e2e_body=e2e_body, lo=sh.lo, rows=sh.rows, n_cols=sh.n_cols,
+            nnz_loc=int(sh.rowptr[-1]),
+            launches=(launches(run.A_own) + (1 if run.A_rem is not None else 0)) if overlap
+            else launches(run.A),
+            moved=(world - 1) * sh.n_max * K * 4, keep=run,
+            desc=("async all_gather_into_tensor(B) || own-column block SpMM, then "
+                  "remote-column block pspmm_spmm_accumulate" if overlap else
+                  "all_gather_into_tensor(B) then pspmm_spmm_run on the local shard"))
 
-    torch.cuda.synchronize()
-    dist.barrier()
-    with torch.cuda.stream(stream):
-        ts = time_steps(step, args.steps, args.warmup, flush, stream, sampler)
-        tk = time_steps(kernel_only, args.steps, 2, flush, stream)
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms, kms = max_over_ranks([float(np.mean(ts)), float(np.mean(tk))])
-    R = algorithmic_bytes(rows, n_cols, nnz_loc, K)
-    # e2e: pinned host B rows of this rank -> device, exchange, SpMM, D2H of its C rows
+    results, head_leg = {}, None
+    for i, kind in enumerate(legs):
+        leg = setup(kind)
+        if isinstance(leg, str):
+            results[kind] = {"unavailable": leg}
+            continue
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        with torch.cuda.stream(stream):
+            ts = time_steps(leg["step"], args.steps, args.warmup, flush, stream,
+                            sampler if head_leg is None else None)
+            tk = time_steps(leg["kernel_only"], args.steps, 2, flush, stream)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        ms, kms = max_over_ranks([float(np.mean(ts)), float(np.mean(tk))])
+        R = algorithmic_bytes(leg["rows"], leg["n_cols"], leg["nnz_loc"], K)
+        (Rmax, moved_max) = max_over_ranks([float(R), float(leg["moved"])])
+        results[kind] = {"ms": ms, "kernel_ms_max": kms,
+                         "gflops": 2.0 * g.nnz * K / (ms * 1e-3) / 1e9,
+                         "exchange_bytes_per_rank_max": int(moved_max),
+                         "shard_algorithmic_bytes_max": int(Rmax),
+                         "kernel_roofline_gbs": Rmax / (kms * 1e-3) / 1e9,
+                         "launches_per_step": leg["launches"], "desc": leg["desc"]}
+        if head_leg is None:
+            head_leg = (kind, leg, ms, kms, Rmax)
+        else:
+            del leg
+    if head_leg is None:
+        raise RuntimeError(f"no exchange leg available: {results}")
+    kind, leg, ms, kms, R = head_leg
+    lo, rows = leg["lo"], leg["rows"]
+    # e2e of the headline leg: pinned host B rows of this rank -> device,
+    # exchange, SpMM, D2H of its C rows
     hB = torch.from_numpy(B[lo:lo + rows].copy()).pin_memory()
     hC = torch.empty((rows, K)).pin_memory()
     with torch.cuda.stream(stream):
-        te = time_steps(lambda: e2e_body(hB, hC), max(3, min(args.steps, 10)), 2, flush, stream)
+        te = time_steps(lambda: leg["e2e_body"](hB, hC), max(3, min(args.steps, 10)), 2, flush,
+                        stream)
     (me,) = max_over_ranks([float(np.mean(te))])
     e2e = {"value": 2.0 * g.nnz * K / (me * 1e-3) / 1e9, "unit": "GFLOP/s",
            "h2d_bytes_per_step": int(hB.numel() * 4), "d2h_bytes_per_step": int(hC.numel() * 4),
-           "ms_per_step": me, "path": "rank shard: H2D B rows, exchange, spmm, D2H C rows"}
-    head = {"shard_rows": rows, "shard_nnz": nnz_loc, "kernel_ms_max": kms,
-            "exchange": "fanout" if fanout is not None else "halo" if use_halo else "allgather",
-            "halo_fraction_max": frac, "step_desc": desc}
-    if fanout_note:
-        head["fanout_note"] = fanout_note
-    return head, ms, kms, R, cfg.as_dict(), A_launch * args.steps, e2e
+           "ms_per_step": me, "path": f"rank shard ({kind}): H2D B rows, exchange, spmm, D2H C rows"}
+    head = {"shard_rows": rows, "shard_nnz": leg["nnz_loc"], "kernel_ms_max": kms,
+            "exchange": kind, "halo_fraction_max": frac, "step_desc": leg["desc"],
+            "exchange_legs": results}
+    return head, ms, kms, R, cfg.as_dict(), leg["launches"] * args.steps, e2e
 
 
 EXCHANGE_DESC = {

@@ -76,6 +76,8 @@ typedef enum {
  *     4 = short-row stream with cp.async shared-memory rings: a row group
  *     owns a contiguous row range and streams its vectors, B rows of 3
  *     batches ahead in flight (same constraints as 3; W, F, G apply);
+ *     5 = row blocks with shared-memory B reuse (pspmm_pcsr_attach_blocks;
+ *     V = 1, S = 0, K % 128 == 0; W, F, G, order do not apply);
  *     1 = dense-panel tensor-core path: the dense 128 x 32 tiles attached by
  *     pspmm_pcsr_attach_dense run on tcgen05 (kind::tf32, 3xTF32 split,
  *     fp32 accumulators in TMEM), the remaining nonzeros on the mode-0
@@ -260,6 +262,42 @@ pspmm_status pspmm_pcsr_attach_dense(pspmm_pcsr A, const int32_t *d_rowptr,
  * min_frac in [0, 1] else INVALID_ARG.
  */
 pspmm_status pspmm_decide_dense(pspmm_pcsr A, int32_t K, double min_frac, pspmm_config *cfg);
+
+/*
+ * (a6: the paper's blocking "to exploit B's data reuse through registers or
+ * shared memory", §3.1) Engine mode 5: row blocks with
+ * shared-memory B reuse.  Rows are grouped in blocks of 128; each block's
+ * columns are cut into windows of 128 B rows, and a CTA stages every window
+ * its block touches (128 B rows x 128 columns of B, one 2-D TMA copy) into
+ * shared memory once, then all the block's nonzeros in that window read it
+ * there instead of gathering their B row from L2.
+ *
+ * pspmm_block_reuse: the reuse that staging would capture, computed on the
+ * device from A's CSR order (V = 1, S = 0 handle, else UNSUPPORTED):
+ * *reuse = nnz / (sum over row blocks of touched windows x 128), i.e. how
+ * many nonzeros read each staged B row.  Synchronises `stream`.
+ *
+ * pspmm_pcsr_attach_blocks: build the mode-5 pack (host pass over A's CSR,
+ * then uploaded; 8 B per nonzero + ~0.2 KB per touched window): per row
+ * block a degree-balanced assignment of its rows to 16 warps x 8 slots, the
+ * touched windows, and the nonzeros reordered window-major.  Derived data:
+ * A's PCSR arrays are untouched; replaces a previous pack; freed by
+ * pspmm_pcsr_destroy.  *out_windows (may be NULL) = touched windows.
+ * Synchronises `stream`.  UNSUPPORTED unless V = 1, S = 0.
+ *
+ * pspmm_decide_blocks (host, pure given the handle): cfg->mode = 5 iff a
+ * pack is attached, K % 128 == 0 and its reuse >= min_reuse; otherwise a
+ * mode of 5 is reset to 0 and any other mode is left alone.
+ *
+ * Mode-5 runs (pspmm_spmm_run / _accumulate / _fanout / the host entries,
+ * which run it whole) need the pack, K % 128 == 0, ld % 4 == 0 and 16-B
+ * aligned B and C, else PSPMM_ERR_UNSUPPORTED; W, F, G and order do not
+ * apply.  Every C element has one writer (no atomics), so results are
+ * deterministic run to run.
+ */
+pspmm_status pspmm_block_reuse(pspmm_pcsr A, void *stream, double *reuse);
+pspmm_status pspmm_pcsr_attach_blocks(pspmm_pcsr A, void *stream, int64_t *out_windows);
+pspmm_status pspmm_decide_blocks(pspmm_pcsr A, int32_t K, double min_reuse, pspmm_config *cfg);
 
 /* Sizes of the attached split (zeros when none): 128-row panels with dense
  * tiles, dense tiles, nonzeros inside them. */

@@ -90,11 +90,13 @@ def _csr(rowptr, colidx, val):
     return rowptr, colidx, val
 
 
-def spmm(rowptr, colidx, val, B, rows=None, threads: int = 1):
+def spmm(rowptr, colidx, val, B, rows=None, threads: int = 1, with_mag: bool = True):
     """c-1: fp64 C = A.B (Alg. 1) and mag = sum |a||b|.
 
     ``rows``: optional int64 array of matrix rows to compute (sampled checks
-    at full size); output row r is matrix row rows[r].
+    at full size); output row r is matrix row rows[r].  ``with_mag=False``
+    skips the tolerance bound (mag is returned as None): the plain product,
+    as bench.py's cpu_baseline times it.
     """
     rowptr, colidx, val = _csr(rowptr, colidx, val)
     B = np.ascontiguousarray(B, dtype=np.float32)
@@ -106,7 +108,7 @@ def spmm(rowptr, colidx, val, B, rows=None, threads: int = 1):
     else:
         cnt = n
     out = np.empty((cnt, K), dtype=np.float64)
-    mag = np.empty((cnt, K), dtype=np.float64)
+    mag = np.empty((cnt, K), dtype=np.float64) if with_mag else None
     st = _L().oracle_spmm_rows(n, _ptr(rowptr), _ptr(colidx), _ptr(val), _ptr(B), K, K,
                                cnt, _ptr(rows), _ptr(out), _ptr(mag), int(threads))
     if st:

@@ -110,6 +110,9 @@ _sig("pspmm_spmm_accumulate", _st, _P, _P, _i64, _i32, _P, _i64, Config, _P)
 _sig("pspmm_pcsr_attach_dense", _st, _P, _P, _P, _P, ctypes.c_double, _i32, _P,
      ctypes.POINTER(_i64))
 _sig("pspmm_decide_dense", _st, _P, _i32, ctypes.c_double, ctypes.POINTER(Config))
+_sig("pspmm_block_reuse", _st, _P, _P, ctypes.POINTER(ctypes.c_double))
+_sig("pspmm_pcsr_attach_blocks", _st, _P, _P, ctypes.POINTER(_i64))
+_sig("pspmm_decide_blocks", _st, _P, _i32, ctypes.c_double, ctypes.POINTER(Config))
 _sig("pspmm_pcsr_dense_info", _st, _P, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
      ctypes.POINTER(_i64))
 _sig("pspmm_spmm_run_host_batch", _st, _P, _P, _i64, _i32, _P, _i64, _i32, Config, _P, _P, _P)
@@ -321,6 +324,30 @@ def pspmm_decide_dense(A: Pcsr, K: int, min_frac: float, cfg: Config) -> Config:
     out = Config(**cfg.as_dict())
     _check(_lib.pspmm_decide_dense(A.handle, K, float(min_frac), ctypes.byref(out)),
            "pspmm_decide_dense")
+    return out
+
+
+def pspmm_block_reuse(A: Pcsr, stream=None) -> float:
+    """Engine mode 5: nonzeros per staged B row (device-computed, V1 S0 handle)."""
+    r = ctypes.c_double()
+    _check(_lib.pspmm_block_reuse(A.handle, _stream(stream), ctypes.byref(r)), "pspmm_block_reuse")
+    return r.value
+
+
+def pspmm_pcsr_attach_blocks(A: Pcsr, stream=None) -> int:
+    """Build the mode-5 pack (row blocks of 128, windows of 128 B rows);
+    returns the number of touched windows."""
+    w = _i64()
+    _check(_lib.pspmm_pcsr_attach_blocks(A.handle, _stream(stream), ctypes.byref(w)),
+           "pspmm_pcsr_attach_blocks")
+    return w.value
+
+
+def pspmm_decide_blocks(A: Pcsr, K: int, min_reuse: float, cfg: Config) -> Config:
+    """Mode-5 rule of the C library (include/pspmm.h); returns a new Config."""
+    out = Config(**cfg.as_dict())
+    _check(_lib.pspmm_decide_blocks(A.handle, K, float(min_reuse), ctypes.byref(out)),
+           "pspmm_decide_blocks")
     return out
 
 
@@ -607,6 +634,31 @@ def auto_dense(A: Pcsr, rowptr, colidx, val, K, cfg: Config, stream=None):
     cfg = pspmm_decide_dense(A, K, DENSE_MIN_FRAC, cfg)
     info.update(min_density=DENSE_MIN_DENSITY, min_frac=DENSE_MIN_FRAC, taken=cfg.mode == 1)
     return cfg, info
+
+
+BLOCK_MIN_REUSE = 2.0
+
+
+def auto_blocks(A: Pcsr, rowptr, colidx, val, K, cfg: Config, stream=None):
+    """Engine mode 5 when the row blocks' staged B rows would be reused
+    enough (K % 128 == 0): returns (cfg, handle to run, info or None).  The
+    reuse is measured on a V = 1, S = 0 handle (A itself when it is one)."""
+    if K % 128 != 0 or cfg.mode == 1:
+        return cfg, A, None
+    H = A
+    if not (A.V == 1 and A.info["S"] == 0):
+        H = pspmm_pcsr_build(A.n_rows, int(colidx.shape[0]), rowptr, colidx, val, 1, 0,
+                             stream=stream, n_cols=A.n_cols)
+    reuse = pspmm_block_reuse(H, stream)
+    info = {"reuse": reuse, "min_reuse": BLOCK_MIN_REUSE, "taken": False}
+    if reuse < BLOCK_MIN_REUSE:
+        return cfg, A, info
+    info["windows"] = pspmm_pcsr_attach_blocks(H, stream)
+    c = Config(**cfg.as_dict())
+    c.V, c.S = 1, 0
+    c = pspmm_decide_blocks(H, K, BLOCK_MIN_REUSE, c)
+    info["taken"] = c.mode == 5
+    return (c, H, info) if c.mode == 5 else (cfg, A, info)
 
 
 def spmm(rowptr, colidx, val, B, cfg: Config | None = None, stream=None, C=None):

@@ -195,6 +195,7 @@ void pspmm_pcsr_destroy(pspmm_pcsr A) {
       if (e) cudaEventDestroy(e);
   if (A->batch_start) cudaEventDestroy(A->batch_start);
   destroy_dense(A->dense);
+  destroy_blocks(A->blocks);
   delete A;
 }
 
@@ -432,6 +433,35 @@ pspmm_status pspmm_pcsr_dense_info(pspmm_pcsr A, int64_t *num_panels, int64_t *n
     *num_panels = A->dense ? A->dense->num_panels : 0;
     *num_tiles = A->dense ? A->dense->num_tiles : 0;
     *nnz_dense = A->dense ? A->dense->nnz_dense : 0;
+    return PSPMM_OK;
+  });
+}
+
+pspmm_status pspmm_block_reuse(pspmm_pcsr A, void *stream, double *reuse) {
+  return pspmm::guarded("block_reuse", [&]() -> pspmm_status {
+    return block_reuse(A, as_stream(stream), reuse, nullptr);
+  });
+}
+
+pspmm_status pspmm_pcsr_attach_blocks(pspmm_pcsr A, void *stream, int64_t *out_windows) {
+  return pspmm::guarded("pcsr_attach_blocks", [&]() -> pspmm_status {
+    pspmm_status st = attach_blocks(A, as_stream(stream));
+    if (st == PSPMM_OK && out_windows) *out_windows = A->blocks->num_windows;
+    return st;
+  });
+}
+
+pspmm_status pspmm_decide_blocks(pspmm_pcsr A, int32_t K, double min_reuse, pspmm_config *cfg) {
+  return pspmm::guarded("decide_blocks", [&]() -> pspmm_status {
+    if (!A || !cfg || K < 1 || !(min_reuse >= 0.0)) {
+      set_error("decide_blocks: null argument, K < 1 or min_reuse < 0");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    if (A->blocks && A->V == 1 && A->S == 0 && K % 128 == 0 && A->nnz > 0 &&
+        A->blocks->reuse >= min_reuse)
+      cfg->mode = 5;
+    else if (cfg->mode == 5)
+      cfg->mode = 0;
     return PSPMM_OK;
   });
 }

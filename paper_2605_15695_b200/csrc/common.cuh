@@ -32,6 +32,21 @@ struct DenseTiles {
   pspmm_features rest_f{};         // Table-3 features of the rest
   bool rest_f_ok = false;
 };
+// Engine mode 5 (spmm_block.cu): rows in blocks of kBlockRows, each block's
+// nonzeros packed window-major (windows of kBlockWindow B rows), attached by
+// pspmm_pcsr_attach_blocks.  Derived data, not part of the PCSR contract.
+constexpr int kBlockRows = 128;
+constexpr int kBlockWindow = 128;
+struct RowBlocks {
+  int64_t num_blocks = 0, num_windows = 0;
+  double reuse = 0.0;              // nnz / (touched windows x kBlockWindow)
+  int32_t *d_win_ptr = nullptr;    // num_blocks + 1
+  int32_t *d_win_c0 = nullptr;     // num_windows
+  uint2 *d_win_cnt = nullptr;      // num_windows x 16 warps: 8 u8 slot counts
+  int32_t *d_win_base = nullptr;   // num_windows x 16 warps
+  int2 *d_pairs = nullptr;         // nnz: (column - window start, value bits)
+  int16_t *d_rowmap = nullptr;     // num_blocks x 16 x 8: local row of each slot
+};
 struct pspmm_pcsr_s {
   int64_t n_rows = 0, n_cols = 0, num_panels = 0, nnz = 0, nnz_v = 0, num_chunks = 0;
   int64_t sg = 0, rowptr_len = 0, num_split = 0;
@@ -52,6 +67,7 @@ struct pspmm_pcsr_s {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {}, batch_start = nullptr;
   DenseTiles *dense = nullptr;         // engine mode 1 (pspmm_pcsr_attach_dense)
+  RowBlocks *blocks = nullptr;         // engine mode 5 (pspmm_pcsr_attach_blocks)
 };
 
 namespace pspmm {
@@ -130,6 +146,17 @@ pspmm_status attach_dense(pspmm_pcsr_s *A, const int32_t *d_rowptr, const int32_
                           const float *d_val, double min_density, int32_t k_max,
                           cudaStream_t stream, int64_t *out_tiles);
 void destroy_dense(DenseTiles *D);
+
+// spmm_block.cu (engine mode 5)
+pspmm_status block_reuse(const pspmm_pcsr_s *A, cudaStream_t stream, double *reuse,
+                         int64_t *touched);
+pspmm_status attach_blocks(pspmm_pcsr_s *A, cudaStream_t stream);
+void destroy_blocks(RowBlocks *B);
+bool block_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc,
+                     const float *d_B, const float *d_C);
+pspmm_status run_spmm_block(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
+                            float *d_C, int64_t ldc, cudaStream_t stream, int32_t accumulate,
+                            const Fanout &fan);
 
 // spmm.cu
 pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,

@@ -36,6 +36,20 @@ def test_bench_single_gpu_line():
     assert set(out["roofline"]) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
     assert set(out["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
     assert out["cpu_baseline"]["kind"] == "oracle" and out["cpu_baseline"]["cores"] >= 1
+    assert "with_mag=False" in out["cpu_baseline"]["sample"]
+    # the compact per-workload summary is the line's LAST key (the driver keeps the tail)
+    assert list(out)[-1] == "summary" and out["summary"][0]["w"] == "cora"
+    assert out["summary"][0]["warm_ms"] > 0
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    import torch
+    n = torch.cuda.device_count() + 1
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", str(n), "--workload", "cora"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300,
+                       env={k: v for k, v in os.environ.items() if k != "WORLD_SIZE"})
+    assert r.returncode != 0 and "refusing" in r.stderr
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
 
 
 @pytest.mark.parametrize("exchange,port", [("allgather", 29533), ("halo", 29534)])
@@ -47,6 +61,22 @@ def test_bench_two_rank_rehearsal_gloo(exchange, port):
     assert out["n_gpus"] == 2 and out["value"] > 0
     assert "row shards" in out["config"]["parallelism"]
     assert ("halo" in out["config"]["parallelism"]) == (exchange == "halo")
+    assert list(out["summary"]["exchange_legs"]) == [exchange]
+    assert out["roofline"]["traffic"] is None  # no 1-GPU ncu figure on a shard
+
+
+def test_bench_two_rank_auto_times_both_legs():
+    """--exchange auto on a dense-halo graph: the all-gather (row e, headline)
+    and the epilogue fan-out (f2 i) are both timed and reported."""
+    out = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                "--master-addr", "127.0.0.1", "--master-port", "29535", "bench.py",
+                "--workload", "cora", "--steps", "3", "--warmup", "3", "--headline-only",
+                "--dist-backend", "gloo"])
+    legs = out["summary"]["exchange_legs"]
+    assert list(legs) == ["allgather", "fanout"]
+    for k in ("allgather", "fanout"):
+        assert legs[k]["ms"] > 0 and legs[k]["kernel_ms_max"] > 0, legs
+        assert legs[k]["exchange_bytes_per_rank_max"] > 0
 
 
 def test_bench_reference_arm():

@@ -42,6 +42,9 @@ def test_full_config(name):
     cfg, dense = api.auto_dense(A, rp, ci, vl, K, cfg)  # engine mode 1 rule, as bench.py
     if name == "proteins_clustered":
         assert cfg.mode == 1 and dense["nnz_dense"] > 0.3 * g.nnz
+    cfg, A, blocks = api.auto_blocks(A, rp, ci, vl, K, cfg)  # engine mode 5 rule, as bench.py
+    if name == "proteins":
+        assert cfg.mode == 5 and blocks["taken"], blocks
     # SpMM, sampled rows (every row for Cora)
     B = gen.config_B(name, g.n)
     Bd = torch.from_numpy(B).cuda()

@@ -35,6 +35,8 @@ def main():
     if a.sg is not None:
         cfg.sg_override = a.sg
     A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, cfg.V, cfg.S, cfg.omega, cfg.sg_override)
+    if cfg.mode == 5:
+        print("blocks: windows", api.pspmm_pcsr_attach_blocks(A))
     if a.dense > 0:
         print(api.pspmm_pcsr_attach_dense(A, rp, ci, vl, a.dense, k_max=g.K))
         cfg.mode = 1
