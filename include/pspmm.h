@@ -266,24 +266,31 @@ pspmm_status pspmm_decide_dense(pspmm_pcsr A, int32_t K, double min_frac, pspmm_
 /*
  * (a6: the paper's blocking "to exploit B's data reuse through registers or
  * shared memory", §3.1) Engine mode 5: row blocks with
- * shared-memory B reuse.  Rows are grouped in blocks of 128; each block's
+ * shared-memory B reuse.  Rows are grouped in blocks of nw x rw rows (nw
+ * consumer warps of rw rows each; 23 x 8 = 184 rows by default); each block's
  * columns are cut into windows of 128 B rows, and a CTA stages every window
  * its block touches (128 B rows x 128 columns of B, one 2-D TMA copy) into
  * shared memory once, then all the block's nonzeros in that window read it
  * there instead of gathering their B row from L2.
  *
- * pspmm_block_reuse: the reuse that staging would capture, computed on the
- * device from A's CSR order (V = 1, S = 0 handle, else UNSUPPORTED):
- * *reuse = nnz / (sum over row blocks of touched windows x 128), i.e. how
- * many nonzeros read each staged B row.  Synchronises `stream`.
+ * pspmm_block_reuse: the reuse that staging would capture, a graph feature
+ * computed on the device from A's CSR order (V = 1, S = 0 handle, else
+ * UNSUPPORTED) on fixed 128-row blocks: *reuse = nnz / (sum over 128-row
+ * blocks of touched windows x 128), i.e. how many nonzeros read each staged
+ * B row.  Synchronises `stream`.
  *
  * pspmm_pcsr_attach_blocks: build the mode-5 pack (host pass over A's CSR,
  * then uploaded; 8 B per nonzero + ~0.2 KB per touched window): per row
- * block a degree-balanced assignment of its rows to 16 warps x 8 slots, the
- * touched windows, and the nonzeros reordered window-major.  Derived data:
- * A's PCSR arrays are untouched; replaces a previous pack; freed by
- * pspmm_pcsr_destroy.  *out_windows (may be NULL) = touched windows.
- * Synchronises `stream`.  UNSUPPORTED unless V = 1, S = 0.
+ * block a degree-balanced assignment of its rows to nw warps x rw slots, the
+ * touched windows (split into virtual windows of at most 1408 nonzeros), and
+ * the nonzeros reordered window by window, warp by warp, slot by slot (runs
+ * padded to an even length).  Derived data: A's PCSR arrays are untouched; replaces a
+ * previous pack; freed by pspmm_pcsr_destroy.  *out_windows (may be NULL) =
+ * touched (block, window) pairs.  Synchronises `stream`.  UNSUPPORTED unless
+ * V = 1, S = 0.
+ *
+ * pspmm_block_info: the attached pack's block height (rows per block) and
+ * touched (block, window) pairs; zeros when no pack is attached.
  *
  * pspmm_decide_blocks (host, pure given the handle): cfg->mode = 5 iff a
  * pack is attached, K % 128 == 0 and its reuse >= min_reuse; otherwise a
@@ -298,6 +305,7 @@ pspmm_status pspmm_decide_dense(pspmm_pcsr A, int32_t K, double min_frac, pspmm_
 pspmm_status pspmm_block_reuse(pspmm_pcsr A, void *stream, double *reuse);
 pspmm_status pspmm_pcsr_attach_blocks(pspmm_pcsr A, void *stream, int64_t *out_windows);
 pspmm_status pspmm_decide_blocks(pspmm_pcsr A, int32_t K, double min_reuse, pspmm_config *cfg);
+pspmm_status pspmm_block_info(pspmm_pcsr A, int32_t *block_rows, int64_t *windows);
 
 /* Sizes of the attached split (zeros when none): 128-row panels with dense
  * tiles, dense tiles, nonzeros inside them. */

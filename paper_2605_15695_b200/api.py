@@ -113,6 +113,7 @@ _sig("pspmm_decide_dense", _st, _P, _i32, ctypes.c_double, ctypes.POINTER(Config
 _sig("pspmm_block_reuse", _st, _P, _P, ctypes.POINTER(ctypes.c_double))
 _sig("pspmm_pcsr_attach_blocks", _st, _P, _P, ctypes.POINTER(_i64))
 _sig("pspmm_decide_blocks", _st, _P, _i32, ctypes.c_double, ctypes.POINTER(Config))
+_sig("pspmm_block_info", _st, _P, ctypes.POINTER(_i32), ctypes.POINTER(_i64))
 _sig("pspmm_pcsr_dense_info", _st, _P, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
      ctypes.POINTER(_i64))
 _sig("pspmm_spmm_run_host_batch", _st, _P, _P, _i64, _i32, _P, _i64, _i32, Config, _P, _P, _P)
@@ -335,12 +336,19 @@ def pspmm_block_reuse(A: Pcsr, stream=None) -> float:
 
 
 def pspmm_pcsr_attach_blocks(A: Pcsr, stream=None) -> int:
-    """Build the mode-5 pack (row blocks of 128, windows of 128 B rows);
-    returns the number of touched windows."""
+    """Build the mode-5 pack (row blocks of 15 x rw rows, windows of 128 B
+    rows); returns the number of touched (block, window) pairs."""
     w = _i64()
     _check(_lib.pspmm_pcsr_attach_blocks(A.handle, _stream(stream), ctypes.byref(w)),
            "pspmm_pcsr_attach_blocks")
     return w.value
+
+
+def pspmm_block_info(A: Pcsr) -> tuple:
+    """(rows per block, touched windows) of the attached mode-5 pack."""
+    r, w = _i32(), _i64()
+    _check(_lib.pspmm_block_info(A.handle, ctypes.byref(r), ctypes.byref(w)), "pspmm_block_info")
+    return r.value, w.value
 
 
 def pspmm_decide_blocks(A: Pcsr, K: int, min_reuse: float, cfg: Config) -> Config:

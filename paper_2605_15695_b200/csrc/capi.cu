@@ -451,6 +451,18 @@ pspmm_status pspmm_pcsr_attach_blocks(pspmm_pcsr A, void *stream, int64_t *out_w
   });
 }
 
+pspmm_status pspmm_block_info(pspmm_pcsr A, int32_t *block_rows, int64_t *windows) {
+  return pspmm::guarded("block_info", [&]() -> pspmm_status {
+    if (!A || !block_rows || !windows) {
+      set_error("block_info: null argument");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    *block_rows = A->blocks ? A->blocks->nw * A->blocks->rw : 0;
+    *windows = A->blocks ? A->blocks->num_windows : 0;
+    return PSPMM_OK;
+  });
+}
+
 pspmm_status pspmm_decide_blocks(pspmm_pcsr A, int32_t K, double min_reuse, pspmm_config *cfg) {
   return pspmm::guarded("decide_blocks", [&]() -> pspmm_status {
     if (!A || !cfg || K < 1 || !(min_reuse >= 0.0)) {

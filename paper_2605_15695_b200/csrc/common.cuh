@@ -32,20 +32,30 @@ struct DenseTiles {
   pspmm_features rest_f{};         // Table-3 features of the rest
   bool rest_f_ok = false;
 };
-// Engine mode 5 (spmm_block.cu): rows in blocks of kBlockRows, each block's
-// nonzeros packed window-major (windows of kBlockWindow B rows), attached by
+// Engine mode 5 (spmm_block.cu): rows in blocks of nw x rw rows (nw
+// consumer warps of rw rows: 23 x 8 by default, 19 x 8, 15 x 8 or 15 x 16
+// for A/B); each block's touched windows of
+// kBlockWindow B rows, split into "virtual windows" of at most
+// kBlockMaxPairs nonzeros; per virtual window its nonzeros packed warp by
+// warp, slot by slot (one bulk copy stages them), attached by
 // pspmm_pcsr_attach_blocks.  Derived data, not part of the PCSR contract.
-constexpr int kBlockRows = 128;
-constexpr int kBlockWindow = 128;
+constexpr int kBlockWindow = 128;     // B rows per staged window
+constexpr int kBlockRw = 8;           // default rows per consumer warp
+constexpr int kBlockNw = 23;          // default consumer warps (8 x 23 = 184-row blocks)
+constexpr int kBlockMaxPairs = 1408;  // nonzeros staged per virtual window (11 KB)
+constexpr int kReuseRows = 128;       // row-block height of the reuse feature
 struct RowBlocks {
-  int64_t num_blocks = 0, num_windows = 0;
+  int64_t num_blocks = 0, num_windows = 0, num_virtual = 0;
+  int32_t rw = 8;                  // rows per consumer warp
+  int32_t nw = 23;                 // consumer warps; block rows = nw * rw
   double reuse = 0.0;              // nnz / (touched windows x kBlockWindow)
-  int32_t *d_win_ptr = nullptr;    // num_blocks + 1
-  int32_t *d_win_c0 = nullptr;     // num_windows
-  uint2 *d_win_cnt = nullptr;      // num_windows x 16 warps: 8 u8 slot counts
-  int32_t *d_win_base = nullptr;   // num_windows x 16 warps
-  int2 *d_pairs = nullptr;         // nnz: (column - window start, value bits)
-  int16_t *d_rowmap = nullptr;     // num_blocks x 16 x 8: local row of each slot
+  int32_t *d_win_ptr = nullptr;    // num_blocks + 1: virtual-window range of each block
+  int32_t *d_win_c0 = nullptr;     // num_virtual: first B row of the window
+  int64_t *d_win_pbase = nullptr;  // num_virtual + 1: first packed pair (even: 16-B aligned)
+  uint8_t *d_win_cnt = nullptr;    // num_virtual x nw x rw: per (window, warp, slot) count
+  uint16_t *d_win_woff = nullptr;  // num_virtual x nw: a warp's first pair in the window
+  int2 *d_pairs = nullptr;         // (column - window start, value bits), windows padded to even
+  int16_t *d_rowmap = nullptr;     // num_blocks x nw x rw: local row of a slot, -1 = none
 };
 struct pspmm_pcsr_s {
   int64_t n_rows = 0, n_cols = 0, num_panels = 0, nnz = 0, nnz_v = 0, num_chunks = 0;

@@ -1,6 +1,6 @@
 """(a6, "B's data reuse through ... shared memory") Engine mode 5 — row
-blocks of 128 with every touched 128-row window of B staged in shared memory
-by TMA — against the fp64 oracle (c-1 bound, every element), the
+blocks of 15 x rw rows with every touched 128-row window of B staged in
+shared memory by TMA — against the fp64 oracle (c-1 bound, every element), the
 device-computed reuse against its definition written out in numpy, the rule,
 and the error surface (include/pspmm.h, pspmm_pcsr_attach_blocks)."""
 import numpy as np
@@ -12,10 +12,10 @@ from gpu_util import assert_parity, dev, oracle_ref
 pytestmark = pytest.mark.gpu
 
 
-def _reuse_def(g, n_cols=None):
-    """nnz / (sum over 128-row blocks of touched 128-column windows x 128)."""
+def _reuse_def(g, block_rows=128):
+    """nnz / (sum over row blocks of touched 128-column windows x 128)."""
     rows = np.repeat(np.arange(g.n), np.diff(g.rowptr))
-    key = (rows // 128).astype(np.int64) * (1 << 32) + g.colidx // 128
+    key = (rows // block_rows).astype(np.int64) * (1 << 32) + g.colidx // 128
     touched = len(np.unique(key))
     return g.nnz / (touched * 128.0) if touched else 0.0, touched
 
@@ -70,8 +70,26 @@ def test_block_engine_parity(name, K):
     A, windows, B, C, _, _ = _run(g, K)
     ref, mag = oracle_ref(g, B)
     assert_parity(C, ref, mag, f"mode 5 {name} K={K}")
-    r, touched = _reuse_def(g)
+    from paper_2605_15695_b200 import api
+    rows, w = api.pspmm_block_info(A)
+    assert rows in (120, 152, 184, 240) and w == windows
+    r, touched = _reuse_def(g, rows)
     assert windows == touched
+
+
+@pytest.mark.parametrize("rw,nw", [("16", "15"), ("8", "19"), ("8", "15")])
+@pytest.mark.parametrize("name", ["clustered_small", "giant_row", "empty_rows", "full_window"])
+def test_block_engine_instances(name, rw, nw, monkeypatch):
+    """The other kernel instances (rows per warp x consumer warps), chosen by
+    the tools' A/B knobs."""
+    monkeypatch.setenv("PSPMM_BLOCK_RW", rw)
+    monkeypatch.setenv("PSPMM_BLOCK_NW", nw)
+    g = GRAPHS[name]()
+    A, windows, B, C, _, _ = _run(g, 128)
+    from paper_2605_15695_b200 import api
+    assert api.pspmm_block_info(A)[0] == int(rw) * int(nw)
+    ref, mag = oracle_ref(g, B)
+    assert_parity(C, ref, mag, f"mode 5 rw={rw} nw={nw} {name}")
 
 
 @pytest.mark.parametrize("name", ["proteins_small", "uniform", "empty_rows"])
@@ -98,8 +116,10 @@ def test_block_engine_rectangular_and_deterministic():
     rng = np.random.default_rng(12)
     n, nc = 333, 1000
     m = rng.random((n, nc)) < 0.05
-    r, c = np.nonzero(m)
-    rp, ci = gen.csr_from_pairs(n, r.astype(np.int64), c.astype(np.int64))
+    r, c = np.nonzero(m)  # row-major: rows ascending, columns ascending within a row
+    rp = np.zeros(n + 1, np.int32)
+    rp[1:] = np.cumsum(np.bincount(r, minlength=n))
+    ci = c.astype(np.int32)
     g = gen.Graph("rect", n, rp, ci, gen.values(int(rp[-1]), 13), 0)
     A, _, B, C, _, outs = _run(g, 128, n_cols=nc, runs=2)
     ref = oracle_ref(g, B)
