@@ -203,6 +203,11 @@ pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64
                                  cudaStream_t stream);
 
 // gnn_layer.cu (f3: the dense product of a GNN layer)
+// gemm_tc.cu (f3 dense product on tcgen05, 3xTF32)
+bool gemm_tc_supported(int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx, const float *d_W,
+                       int64_t ldw, const float *d_T, int64_t ldt);
+pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
+                     const float *d_W, int64_t ldw, float *d_T, int64_t ldt, cudaStream_t stream);
 pspmm_status dense_gemm(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
                         const float *d_W, int64_t ldw, float *d_T, int64_t ldt,
                         cudaStream_t stream);

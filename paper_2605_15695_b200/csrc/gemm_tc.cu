@@ -1,0 +1,310 @@
+// (f3) The dense product of a GNN layer, T = X . W, on the tcgen05 tensor
+// cores (a GCN / GIN layer is H' = A . H . W).
+//
+// X is n x Ki (row major, ldx), W is Ki x Ko (row major, ldw), T is n x Ko.
+// With Ki, Ko ~ 64..256 the product moves 4 n (Ki + Ko) bytes for 2 n Ki Ko
+// flops: 16 flop/B at Ki = Ko = 64, above the B200's FFMA / HBM balance
+// (~11 flop/B), so on CUDA cores it is FFMA-bound (~26 us for Reddit's
+// 233k x 64 x 64); on the tensor cores it is HBM-bound (~18 us).
+//
+// fp32 accuracy with TF32 inputs ("3xTF32"): x = hi + lo with hi = rna(x),
+// lo = rna(x - hi); X.W ~ Xhi.Whi + Xhi.Wlo + Xlo.Whi (the dropped lo.lo
+// term is below 2^-22 relative), accumulated in fp32 in TMEM.
+//
+// One persistent CTA per SM, warp-specialised (9 warps):
+//  - warps 0-3 (loaders): thread r owns row r of the current 128-row tile;
+//    per 32-column chunk of X it loads its 128 contiguous bytes (8 x LDG.128),
+//    splits them and writes hi / lo into a stage in the no-swizzle K-major
+//    core-matrix layout (core matrix = 8 rows x 16 B; consecutive rows 16 B
+//    apart, so the stores are conflict-free), then fence.proxy.async and an
+//    mbarrier arrive; `stages` chunks in flight;
+//  - warp 4 lane 0 (MMA): per chunk 4 K-steps x 3 tcgen05.mma.kind::tf32
+//    (M = 128, N = Ko, K = 8) into one of two TMEM accumulators (2 x Ko
+//    columns), tcgen05.commit frees the stage / publishes the accumulator;
+//  - warps 5-8 (epilogue): tcgen05.ld 32x32b (warp w reads TMEM lanes
+//    32 (w % 4) .. + 31 = rows of the tile), streaming stores of T, then
+//    free the accumulator, so the next tile's MMAs overlap this epilogue.
+//  W's hi / lo image (all of Ki x Ko) is split once per CTA into shared
+//  memory by the loaders before the first tile.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pspmm {
+namespace {
+
+constexpr int kM = 128;                 // rows per tile (MMA M, TMEM lanes)
+constexpr int kKc = 32;                 // X columns per chunk
+constexpr int kChunkPart = kM * kKc * 4;  // one part (hi or lo) of a chunk: 16 KB
+constexpr int kChunkBytes = 2 * kChunkPart;
+constexpr int kLoaders = 128, kEpi = 128;
+constexpr int kThreads = kLoaders + 32 + kEpi;  // 288
+constexpr int kMaxSmem = 227 * 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// UMMA shared-memory descriptor, no swizzle, K-major (as spmm_dense.cu):
+// lbo = bytes between core matrices adjacent along K, sbo = along M / N.
+__device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+// kind::tf32 instruction descriptor: D fp32, A / B TF32, both K-major, M = 128
+__device__ __forceinline__ uint32_t idesc(int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(kM >> 4) << 24);
+}
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void split4(const float4 &x, float4 &hi, float4 &lo) {
+  hi = make_float4(tf32_rn(x.x), tf32_rn(x.y), tf32_rn(x.z), tf32_rn(x.w));
+  lo = make_float4(tf32_rn(x.x - hi.x), tf32_rn(x.y - hi.y), tf32_rn(x.z - hi.z),
+                   tf32_rn(x.w - hi.w));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t id,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+struct GemmArgs {
+  const float *__restrict__ X;
+  const float *__restrict__ W;
+  float *__restrict__ T;
+  int64_t n, ldx, ldw, ldt;
+  int32_t Ki, Ko, stages, tmem_cols;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int Ki = a.Ki, Ko = a.Ko, S = a.stages;
+  const uint32_t wpart = (uint32_t)Ki * Ko * 4;  // one part of W's image
+  uint8_t *wimg = smem;                          // [hi | lo], each [Ki/4][Ko][4]
+  uint8_t *stage0 = smem + 2 * wpart;            // S x [hi 16 KB | lo 16 KB]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(stage0 + (size_t)S * kChunkBytes);
+  uint64_t *full = bar, *empty = bar + S, *accf = bar + 2 * S, *acce = bar + 2 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 2 * S + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tiles = (a.n + kM - 1) / kM;
+  const int chunks = Ki / kKc;
+
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(a.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], kLoaders);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], kEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // W -> hi / lo image: element (k, n) at [k / 4][n][k % 4]
+  if (tid < kLoaders) {
+    const int q = Ko / 4;  // float4 per W row
+    for (int i = tid; i < Ki * q; i += kLoaders) {
+      const int k = i / q, n4 = i % q;
+      const float4 w = *reinterpret_cast<const float4 *>(a.W + (int64_t)k * a.ldw + 4 * n4);
+      float4 hi, lo;
+      split4(w, hi, lo);
+      const float h[4] = {hi.x, hi.y, hi.z, hi.w}, l[4] = {lo.x, lo.y, lo.z, lo.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t off = ((uint32_t)(k >> 2) * Ko + 4 * n4 + e) * 16 + (k & 3) * 4;
+        *reinterpret_cast<float *>(wimg + off) = h[e];
+        *reinterpret_cast<float *>(wimg + wpart + off) = l[e];
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {  // loaders: thread tid owns row tid of each tile
+    int it = 0;    // chunk counter across tiles (stage ring position)
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int64_t row = t * kM + tid;
+      const float *xr = a.X + row * a.ldx;
+      for (int c = 0; c < chunks; ++c, ++it) {
+        const int s = it % S;
+        if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+        uint8_t *st = stage0 + (size_t)s * kChunkBytes;
+        float4 x[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          x[g] = row < a.n ? __ldcs(reinterpret_cast<const float4 *>(xr + c * kKc + 4 * g))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {  // core-matrix layout: [k-group][row][16 B]
+          float4 hi, lo;
+          split4(x[g], hi, lo);
+          *reinterpret_cast<float4 *>(st + g * (kM * 16) + tid * 16) = hi;
+          *reinterpret_cast<float4 *>(st + kChunkPart + g * (kM * 16) + tid * 16) = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&full[s]);
+      }
+    }
+  } else if (warp == 4) {  // MMA issuer
+    if (lane == 0) {
+      const uint32_t id = idesc(Ko);
+      const uint32_t bytes_b = (uint32_t)Ko * 16;  // one K group of W (Ko x 16 B)
+      const uint32_t whi = smem_u32(wimg), wlo = whi + wpart;
+      int it = 0, tl = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        const int b = tl & 1;
+        if (tl >= 2) mbar_wait(&acce[b], ((tl >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)(b * Ko);
+        for (int c = 0; c < chunks; ++c, ++it) {
+          const int s = it % S;
+          mbar_wait(&full[s], (it / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t xhi = smem_u32(stage0 + (size_t)s * kChunkBytes), xlo = xhi + kChunkPart;
+#pragma unroll
+          for (int ks = 0; ks < kKc / 8; ++ks) {
+            const uint32_t oa = ks * 2 * (kM * 16);
+            const uint32_t ob = (uint32_t)(c * (kKc / 4) + 2 * ks) * bytes_b;
+            const uint64_t dah = desc(xhi + oa, kM * 16, 128), dal = desc(xlo + oa, kM * 16, 128);
+            const uint64_t dbh = desc(whi + ob, bytes_b, 128), dbl = desc(wlo + ob, bytes_b, 128);
+            mma_tf32(acc, dah, dbh, id, (c > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32(acc, dah, dbl, id, 1u);
+            mma_tf32(acc, dal, dbh, id, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&accf[b]);
+      }
+    }
+    __syncwarp();
+  } else {  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31
+    const int quarter = warp & 3;
+    int tl = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+      const int b = tl & 1;
+      mbar_wait(&accf[b], (tl >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row = t * kM + quarter * 32 + lane;
+      const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * Ko);
+      for (int c = 0; c < Ko; c += 16) {
+        float v[16];
+        tmem_ld16(tb + c, v);
+        if (row < a.n) {
+          float4 *dst = reinterpret_cast<float4 *>(a.T + row * a.ldt + c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            __stcs(dst + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acce[b]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(a.tmem_cols));
+}
+
+int tmem_cols_for(int Ko) {
+  int c = 32;
+  while (c < 2 * Ko) c <<= 1;
+  return c;
+}
+
+}  // namespace
+
+// Shapes the tensor-core product takes: Ki % 32 == 0, Ko % 16 == 0,
+// 16 <= Ko <= 256, W's hi / lo image plus two X stages in shared memory,
+// 16-B aligned X / W / T with ld % 4 == 0.
+bool gemm_tc_supported(int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx, const float *d_W,
+                       int64_t ldw, const float *d_T, int64_t ldt) {
+  if (Ki < kKc || Ki % kKc != 0 || Ko < 16 || Ko > 256 || Ko % 16 != 0) return false;
+  if (ldx % 4 || ldw % 4 || ldt % 4) return false;
+  if ((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_W) |
+       reinterpret_cast<uintptr_t>(d_T)) & 15)
+    return false;
+  const int64_t w = 2ll * Ki * Ko * 4;
+  return w + 2ll * kChunkBytes + 1024 + 256 <= kMaxSmem;
+}
+
+pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
+                     const float *d_W, int64_t ldw, float *d_T, int64_t ldt, cudaStream_t stream) {
+  if (n == 0) return PSPMM_OK;
+  const int64_t w = 2ll * Ki * Ko * 4;
+  const int stages = (int)std::min<int64_t>(4, (kMaxSmem - 1024 - 256 - w) / kChunkBytes);
+  const size_t smem = (size_t)(w + (int64_t)stages * kChunkBytes + 1024 + 256);
+  PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  GemmArgs args;
+  args.X = d_X;
+  args.W = d_W;
+  args.T = d_T;
+  args.n = n;
+  args.ldx = ldx;
+  args.ldw = ldw;
+  args.ldt = ldt;
+  args.Ki = Ki;
+  args.Ko = Ko;
+  args.stages = stages;
+  args.tmem_cols = tmem_cols_for(Ko);
+  const int64_t tiles = (n + kM - 1) / kM;
+  const int grid = (int)std::min<int64_t>(tiles, num_sms());
+  gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(args);
+  PSPMM_CUDA_TRY(cudaGetLastError());
+  return PSPMM_OK;
+}
+
+}  // namespace pspmm

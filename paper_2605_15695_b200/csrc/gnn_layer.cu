@@ -2,6 +2,10 @@
 // GIN layers are H' = A . H . W): the dense product with the layer weight
 // and the SpMM, ordered so the SpMM runs on the narrower side.
 //
+// dense_gemm: T = X . W.  Shapes the tensor-core product takes (Ki % 32,
+// Ko % 16, Ko <= 256, W's TF32 image in shared memory) run gemm_tc.cu's
+// 3xTF32 tcgen05 kernel; the rest run dense_gemm_kernel below.
+//
 // dense_gemm_kernel: T = X . W in fp32 on CUDA cores.  X is n x Ki (row
 // major, ldx), W is Ki x Ko (row major, ldw), T is n x Ko.  This is an
 // HBM-bound skinny product (Ki, Ko <= 256, n ~ 10^5..10^6: 2 n Ki Ko flops
@@ -12,6 +16,7 @@
 // row, an L1 broadcast) and reusing every W float4 four times.  fp32 with
 // sequential accumulation over Ki (error <= Ki 2^-24 sum |x||w|).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -75,6 +80,12 @@ pspmm_status dense_gemm(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int
   if (!d_X || !d_W || !d_T) PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "dense_gemm: null pointer");
   if (n < 0 || Ki < 1 || Ko < 1 || ldx < Ki || ldw < Ko || ldt < Ko)
     PSPMM_FAIL(PSPMM_ERR_DIM_MISMATCH, "dense_gemm: need Ki, Ko >= 1 and ld >= width");
+  // the tensor-core product (gemm_tc.cu) where its shape rules hold; the
+  // CUDA-core kernel below for every other shape (PSPMM_GEMM_CC=1 forces it,
+  // an A/B knob for the tools)
+  const char *cc = std::getenv("PSPMM_GEMM_CC");
+  if (!(cc && cc[0] == '1') && gemm_tc_supported(Ki, Ko, d_X, ldx, d_W, ldw, d_T, ldt))
+    return gemm_tc(n, Ki, Ko, d_X, ldx, d_W, ldw, d_T, ldt, stream);
   const size_t smem = (size_t)Ki * kTileCols * sizeof(float);
   if (smem > 200 * 1024) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "dense_gemm: Ki > 800");
   if (n == 0) return PSPMM_OK;

@@ -34,8 +34,38 @@ def test_dense_gemm(n, Ki, Ko):
     _check(T.cpu().numpy(), ref, mag, f"gemm {n}x{Ki}x{Ko}")
 
 
+@pytest.mark.parametrize("force_cc", [False, True])
+@pytest.mark.parametrize("n,Ki,Ko,pad", [(1, 32, 16, 0), (127, 64, 64, 0), (128, 64, 64, 0),
+                                         (129, 64, 64, 4), (1000, 128, 128, 0),
+                                         (4097, 256, 64, 0), (3000, 64, 256, 8),
+                                         (20000, 32, 48, 0), (300, 96, 112, 0)])
+def test_dense_gemm_tensor_core_shapes(n, Ki, Ko, pad, force_cc, monkeypatch):
+    """Shapes the tcgen05 3xTF32 product takes (gemm_tc.cu: Ki % 32, Ko % 16,
+    Ko <= 256), ragged tiles (n % 128 != 0), padded leading dimensions; the
+    same shapes forced onto the CUDA-core kernel (PSPMM_GEMM_CC=1).  Both
+    against the fp64 product with the c-1 bound on |X| |W|."""
+    import torch
+    from paper_2605_15695_b200 import api
+    if force_cc:
+        monkeypatch.setenv("PSPMM_GEMM_CC", "1")
+    X = gen.dense(n, Ki, 31)
+    W = gen.dense(Ki, Ko, 32)
+    Xb = torch.zeros((n, Ki + pad), device="cuda")
+    Xb[:, :Ki] = torch.from_numpy(X).cuda()
+    Tb = torch.full((n, Ko + pad), float("nan"), device="cuda")
+    api.pspmm_dense_gemm(Xb[:, :Ki], torch.from_numpy(W).cuda(), Tb[:, :Ko])
+    torch.cuda.synchronize()
+    ref = X.astype(np.float64) @ W.astype(np.float64)
+    mag = np.abs(X.astype(np.float64)) @ np.abs(W.astype(np.float64))
+    T = Tb.cpu().numpy()
+    _check(T[:, :Ko], ref, mag, f"gemm {n}x{Ki}x{Ko} pad {pad} cc={force_cc}")
+    if pad:
+        assert np.isnan(T[:, Ko:]).all(), "padding columns of T were written"
+
+
 @pytest.mark.parametrize("name", ["reddit_s", "roadnet_s", "empty_rows"])
-@pytest.mark.parametrize("Ki,Ko", [(64, 32), (32, 64), (48, 48), (128, 16)])
+@pytest.mark.parametrize("Ki,Ko", [(64, 32), (32, 64), (48, 48), (128, 16), (64, 64),
+                                   (128, 128)])
 def test_gnn_layer(name, Ki, Ko):
     import torch
     from paper_2605_15695_b200 import api

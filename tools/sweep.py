@@ -8,6 +8,11 @@ flushed between launches, like bench.py).  Writes one JSON record per
 
 python tools/sweep.py --workloads reddit,products --out gpurun_out/sweep.json
 python tools/sweep.py --corpus 40 --Ks 16,32,64,128,256 --out gpurun_out/corpus.json
+python tools/sweep.py --recheck profiles/r01/sweeps/sweep_*.json --corpus 60 --top 8 \
+    --iters 21 --out gpurun_out/recheck.json
+    (re-time the top-8 labels of every (graph, K) record, plus the decided
+    config, with 21 launches each, round-robin across the candidates so clock
+    drift hits them alike: the labels' noise check)
 """
 import argparse
 import json
@@ -40,15 +45,18 @@ def lattice(K, Ws=(2, 4, 8), max_passes=16):
     return out
 
 
-def corpus_graphs(count, seed=12345):
-    """Moderate synthetic graphs across generators, exponents and ID orders
-    (decider training corpus; n ~ 2e4 .. 4e5)."""
+def corpus_graphs(count, seed=12345, n_lo=20000, n_hi=400000, prefix=""):
+    """Synthetic graphs across generators, exponents and ID orders (decider
+    training corpus; n ~ 2e4 .. 4e5 by default; the round-2 supplements use
+    n ~ 1e3 .. 2e4 and 8e5 .. 3e6 so the bench graphs' sizes are inside the
+    training range)."""
     import gen
     rng = np.random.default_rng(seed)
     gs = []
     for i in range(count):
         kind = ["powerlaw", "uniform", "banded", "community", "chung_lu", "community_shuffled"][i % 6]
-        n = int(rng.integers(20000, 400000))
+        n = int(np.exp(rng.uniform(np.log(n_lo), np.log(n_hi)))) if n_lo < 20000 or \
+            n_hi > 400000 else int(rng.integers(n_lo, n_hi))
         s = int(rng.integers(1, 1 << 30))
         if kind == "powerlaw":
             g = gen.powerlaw(n, float(rng.uniform(4, 64)), float(rng.uniform(1.8, 3.0)), s)
@@ -60,12 +68,12 @@ def corpus_graphs(count, seed=12345):
             g = gen.community(n, int(rng.choice([32, 128, 512, 2048])), float(rng.uniform(4, 64)),
                               float(rng.uniform(0.5, 0.95)), s, ordered=(kind == "community"))
         else:
-            d = float(min(rng.uniform(4, 200), 2e7 / n))  # keep nnz <= 2e7 (sweep time)
+            d = float(min(rng.uniform(4, 200), 2e7 / n, max(4.0, n / 8.0)))  # nnz <= 2e7
             nnz = int(n * d) // 2 * 2
             rp, ci = gen.chung_lu(n, nnz, int(min(n - 1, d * rng.uniform(10, 60))), s,
                                   shuffle_seed=s + 1)
             g = gen.Graph(f"chunglu_n{n}_d{d:.0f}", n, rp, ci, gen.values(len(ci), s + 2))
-        g.name = f"{i:03d}_{g.name}"
+        g.name = f"{prefix}{i:03d}_{g.name}"
         gs.append(g)
     return gs
 
@@ -129,6 +137,63 @@ def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2,
     return recs
 
 
+def recheck_graph(g, recs, top, iters, flush, stream):
+    """Re-time the `top` fastest table entries of each of g's records (and the
+    currently decided config) with `iters` launches, round-robin."""
+    import torch
+    from paper_2605_15695_b200 import api
+    rp = torch.from_numpy(g.rowptr).cuda()
+    ci = torch.from_numpy(g.colidx).cuda()
+    vl = torch.from_numpy(g.val).cuda()
+    handles = {}
+    out = []
+    for r in recs:
+        K = r["K"]
+        cands = sorted(r["table"], key=lambda t: t["ms"])[:top]
+        d = api.pspmm_decide_config(api.pspmm_features_compute(g.n, g.nnz, rp, ci), K).as_dict()
+        key = lambda t: (t["V"], t["S"], t["W"], t["F"], t["G"], t.get("mode", 0),
+                         t.get("order", 0))
+        if d["mode"] in (0, 2, 3, 4) and key(d) not in {key(t) for t in cands}:
+            cands.append({k: d[k] for k in ("V", "S", "W", "F", "G", "mode", "order")})
+        B = torch.rand((g.n, K), device="cuda") * 2 - 1
+        C = torch.empty((g.n, K), device="cuda")
+        cfgs = []
+        for t in cands:
+            vs = (t["V"], t["S"])
+            if vs not in handles:
+                handles[vs] = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, *vs)
+            cfg = api.Config(W=t["W"], F=max(t["F"], 1), V=t["V"], S=t["S"], G=t["G"],
+                             mode=t.get("mode", 0), order=t.get("order", 0))
+            handles[vs].run(B, C, cfg, stream)  # warm-up / domain check
+            cfgs.append((t, handles[vs], cfg))
+        ts = [[] for _ in cfgs]
+        for _ in range(iters):
+            for j, (t, A, cfg) in enumerate(cfgs):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                flush()
+                e0.record(stream)
+                A.run(B, C, cfg, stream)
+                e1.record(stream)
+                ts[j].append((e0, e1))
+        torch.cuda.synchronize()
+        table = []
+        for (t, _, _), ev in zip(cfgs, ts):
+            ms = [a.elapsed_time(b) for a, b in ev]
+            e = {k: t.get(k, 0) for k in ("V", "S", "W", "F", "G", "mode", "order")}
+            e.update({"ms": float(np.median(ms)), "ms_min": float(np.min(ms)),
+                      "ms_iqr": float(np.percentile(ms, 75) - np.percentile(ms, 25)),
+                      "ms_sweep7": t.get("ms")})
+            table.append(e)
+        best = min(table, key=lambda x: x["ms"])
+        out.append({"graph": r["graph"], "n": r["n"], "nnz": r["nnz"], "K": K,
+                    "features": r["features"], "table": table, "best": best, "recheck": iters,
+                    "decided": d})
+        del B, C
+    del handles
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     import torch
 
@@ -137,6 +202,8 @@ def main():
     ap.add_argument("--workloads", default="")
     ap.add_argument("--corpus", type=int, default=0)
     ap.add_argument("--corpus-seed", type=int, default=12345)
+    ap.add_argument("--corpus-n", default="20000,400000", help="node-count range lo,hi")
+    ap.add_argument("--corpus-prefix", default="")
     ap.add_argument("--Ks", default="")
     ap.add_argument("--iters", type=int, default=7)
     ap.add_argument("--Ws", default="2,4,8")
@@ -144,6 +211,10 @@ def main():
     ap.add_argument("--modes", default="0", help="engine modes to sweep: 0 (LDG), 2 (TMA), 3")
     ap.add_argument("--orders", default="0", help="mode-0 unit orders to sweep: 0, 1")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--recheck", nargs="*", default=None,
+                    help="sweep files whose top labels to re-time (graphs: --workloads names "
+                         "and --corpus N regenerated)")
+    ap.add_argument("--top", type=int, default=8)
     a = ap.parse_args()
     Ws = tuple(int(x) for x in a.Ws.split(","))
     VS = tuple((int(x[0]), int(x[1])) for x in a.VS.split(","))
@@ -157,6 +228,27 @@ def main():
 
     recs = []
     t0 = time.time()
+    if a.recheck:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from train_decider import load
+        old = load(a.recheck)
+        by_graph = {}
+        for r in old:
+            by_graph.setdefault(r["graph"], []).append(r)
+        graphs = []
+        for name in by_graph:
+            if name in bench.WORKLOADS:
+                graphs.append(bench.load_graph(name))
+        for g in corpus_graphs(a.corpus, a.corpus_seed) if a.corpus else []:
+            if g.name in by_graph:
+                graphs.append(g)
+        for g in graphs:
+            recs += recheck_graph(g, sorted(by_graph[g.name], key=lambda r: r["K"]), a.top,
+                                  a.iters, flush, stream)
+            print(f"[{time.time() - t0:.0f}s] recheck {g.name}: {len(recs)} records", flush=True)
+            json.dump(recs, open(a.out, "w"))
+        json.dump(recs, open(a.out, "w"))
+        return
     for name in [w for w in a.workloads.split(",") if w]:
         g = bench.load_graph(name)
         Ks = [int(k) for k in a.Ks.split(",")] if a.Ks else [g.K]
@@ -166,7 +258,8 @@ def main():
         json.dump(recs, open(a.out, "w"))
     if a.corpus:
         Ks = [int(k) for k in a.Ks.split(",")] if a.Ks else [16, 32, 64, 128, 256]
-        for g in corpus_graphs(a.corpus, a.corpus_seed):
+        lo, hi = (int(x) for x in a.corpus_n.split(","))
+        for g in corpus_graphs(a.corpus, a.corpus_seed, lo, hi, a.corpus_prefix):
             recs += sweep_graph(g, Ks, a.iters, flush, stream, Ws, VS, modes, orders)
             print(f"[{time.time() - t0:.0f}s] {g.name} n={g.n} nnz={g.nnz}", flush=True)
             json.dump(recs, open(a.out, "w"))
