@@ -307,6 +307,35 @@ pspmm_status pspmm_pcsr_attach_blocks(pspmm_pcsr A, void *stream, int64_t *out_w
 pspmm_status pspmm_decide_blocks(pspmm_pcsr A, int32_t K, double min_reuse, pspmm_config *cfg);
 pspmm_status pspmm_block_info(pspmm_pcsr A, int32_t *block_rows, int64_t *windows);
 
+/*
+ * (a6 on locality-ordered graphs: the paper's reordering step, P:271-272
+ * §4.4, and its locality argument for blocking) Engine mode 6:
+ * staged bands.  Rows are grouped in blocks of 128; each block's distinct
+ * columns are merged into contiguous ranges of B rows (gaps of <= 8 rows
+ * included), and a CTA stages the whole band with one 1-D bulk copy per
+ * range into shared memory before any row is computed, while its rows'
+ * (slot, value) pairs load into registers; every nonzero then reads its B
+ * row from shared memory.  No per-nonzero dependent global gather remains
+ * on the critical path.
+ *
+ * pspmm_pcsr_attach_band: build the pack (host pass over A's CSR, then
+ * uploaded; 4 B per nonzero + 8 B per range): per block the ranges and each
+ * nonzero's row slot in the band.  k_max (multiple of 4, 4..128) bounds the
+ * K and the B row pitch (ldb) of later runs: a block is staged when its band
+ * fits 64 KB at k_max columns; other blocks keep the column and gather from
+ * global memory.  *staged_frac (may be NULL) = staged / non-empty blocks.
+ * Replaces a previous pack; freed by pspmm_pcsr_destroy.  Synchronises
+ * `stream`.  UNSUPPORTED unless V = 1, S = 0; INVALID_ARG for a bad k_max.
+ *
+ * Mode-6 runs (pspmm_spmm_run / _accumulate / _fanout / the host entries,
+ * which run it whole) need the pack, K % 4 == 0, K <= ldb <= k_max,
+ * ldc % 4 == 0 and 16-B aligned B and C, else PSPMM_ERR_UNSUPPORTED; W, F, G
+ * and order do not apply.  One writer per C element (deterministic).
+ */
+pspmm_status pspmm_pcsr_attach_band(pspmm_pcsr A, int32_t k_max, void *stream,
+                                    double *staged_frac);
+
+
 /* Sizes of the attached split (zeros when none): 128-row panels with dense
  * tiles, dense tiles, nonzeros inside them. */
 pspmm_status pspmm_pcsr_dense_info(pspmm_pcsr A, int64_t *num_panels, int64_t *num_tiles,

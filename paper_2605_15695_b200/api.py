@@ -114,6 +114,7 @@ _sig("pspmm_block_reuse", _st, _P, _P, ctypes.POINTER(ctypes.c_double))
 _sig("pspmm_pcsr_attach_blocks", _st, _P, _P, ctypes.POINTER(_i64))
 _sig("pspmm_decide_blocks", _st, _P, _i32, ctypes.c_double, ctypes.POINTER(Config))
 _sig("pspmm_block_info", _st, _P, ctypes.POINTER(_i32), ctypes.POINTER(_i64))
+_sig("pspmm_pcsr_attach_band", _st, _P, _i32, _P, ctypes.POINTER(ctypes.c_double))
 _sig("pspmm_pcsr_dense_info", _st, _P, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
      ctypes.POINTER(_i64))
 _sig("pspmm_spmm_run_host_batch", _st, _P, _P, _i64, _i32, _P, _i64, _i32, Config, _P, _P, _P)
@@ -349,6 +350,15 @@ def pspmm_block_info(A: Pcsr) -> tuple:
     r, w = _i32(), _i64()
     _check(_lib.pspmm_block_info(A.handle, ctypes.byref(r), ctypes.byref(w)), "pspmm_block_info")
     return r.value, w.value
+
+
+def pspmm_pcsr_attach_band(A: Pcsr, k_max: int, stream=None) -> float:
+    """Build the mode-6 pack (staged bands of 128-row blocks; K, ldb <= k_max);
+    returns the fraction of non-empty blocks whose band is staged."""
+    f = ctypes.c_double()
+    _check(_lib.pspmm_pcsr_attach_band(A.handle, int(k_max), _stream(stream), ctypes.byref(f)),
+           "pspmm_pcsr_attach_band")
+    return f.value
 
 
 def pspmm_decide_blocks(A: Pcsr, K: int, min_reuse: float, cfg: Config) -> Config:

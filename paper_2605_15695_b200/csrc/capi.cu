@@ -196,6 +196,7 @@ void pspmm_pcsr_destroy(pspmm_pcsr A) {
   if (A->batch_start) cudaEventDestroy(A->batch_start);
   destroy_dense(A->dense);
   destroy_blocks(A->blocks);
+  destroy_band(A->band);
   delete A;
 }
 
@@ -460,6 +461,13 @@ pspmm_status pspmm_block_info(pspmm_pcsr A, int32_t *block_rows, int64_t *window
     *block_rows = A->blocks ? A->blocks->nw * A->blocks->rw : 0;
     *windows = A->blocks ? A->blocks->num_windows : 0;
     return PSPMM_OK;
+  });
+}
+
+pspmm_status pspmm_pcsr_attach_band(pspmm_pcsr A, int32_t k_max, void *stream,
+                                    double *staged_frac) {
+  return pspmm::guarded("pcsr_attach_band", [&]() -> pspmm_status {
+    return attach_band(A, k_max, as_stream(stream), staged_frac);
   });
 }
 

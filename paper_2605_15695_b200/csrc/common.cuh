@@ -57,6 +57,23 @@ struct RowBlocks {
   int2 *d_pairs = nullptr;         // (column - window start, value bits), windows padded to even
   int16_t *d_rowmap = nullptr;     // num_blocks x nw x rw: local row of a slot, -1 = none
 };
+// Engine mode 6 (spmm_band.cu): rows in blocks of kBandRows; per block the
+// contiguous ranges of B rows it touches (staged by bulk copies) and every
+// nonzero's slot in that band, attached by pspmm_pcsr_attach_band.  Derived
+// data, not part of the PCSR contract.
+constexpr int kBandRows = 128;
+constexpr int kBandBytes = 64 * 1024;  // staged band budget per block (3 CTAs per SM)
+constexpr int kBandMaxK = 128;
+struct Band {
+  int64_t num_blocks = 0;
+  int32_t k_max = 0;
+  double staged_frac = 0.0;         // non-empty blocks whose band fits the budget
+  int32_t *d_slot = nullptr;        // nnz: band slot (staged block) or column (unstaged)
+  int32_t *d_rng_ptr = nullptr;     // num_blocks + 1
+  int32_t *d_rng_lo = nullptr;      // first B row of each range
+  int32_t *d_rng_len = nullptr;     // rows of each range
+  int32_t *d_blk_rows = nullptr;    // num_blocks: staged rows (-1 over budget, 0 empty)
+};
 struct pspmm_pcsr_s {
   int64_t n_rows = 0, n_cols = 0, num_panels = 0, nnz = 0, nnz_v = 0, num_chunks = 0;
   int64_t sg = 0, rowptr_len = 0, num_split = 0;
@@ -78,6 +95,7 @@ struct pspmm_pcsr_s {
   cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {}, batch_start = nullptr;
   DenseTiles *dense = nullptr;         // engine mode 1 (pspmm_pcsr_attach_dense)
   RowBlocks *blocks = nullptr;         // engine mode 5 (pspmm_pcsr_attach_blocks)
+  Band *band = nullptr;                // engine mode 6 (pspmm_pcsr_attach_band)
 };
 
 namespace pspmm {
@@ -168,6 +186,15 @@ pspmm_status run_spmm_block(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb
                             float *d_C, int64_t ldc, cudaStream_t stream, int32_t accumulate,
                             const Fanout &fan);
 
+// spmm_band.cu (engine mode 6)
+void destroy_band(Band *D);
+pspmm_status attach_band(pspmm_pcsr_s *A, int32_t k_max, cudaStream_t stream, double *staged_frac);
+bool band_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc, const float *d_B,
+                    const float *d_C);
+pspmm_status run_spmm_band(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
+                           float *d_C, int64_t ldc, cudaStream_t stream, int32_t accumulate,
+                           const Fanout &fan);
+
 // spmm.cu
 pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K, float *d_C,
                       int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
@@ -203,6 +230,9 @@ pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64
                                  cudaStream_t stream);
 
 // gnn_layer.cu (f3: the dense product of a GNN layer)
+// spmm_block.cu: cuTensorMapEncodeTiled (PFN_cuTensorMapEncodeTiled_v12000),
+// nullptr when the driver lacks it
+void *tensor_map_encoder();
 // gemm_tc.cu (f3 dense product on tcgen05, 3xTF32)
 bool gemm_tc_supported(int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx, const float *d_W,
                        int64_t ldw, const float *d_T, int64_t ldt);

@@ -9,6 +9,7 @@
 //   F: smallest coarsening whose row group fits in a warp with no MAC-job gap
 //      (Eq. 1 generalised to 4G lanes).
 #include "guard.h"
+#include <algorithm>
 #include <cmath>
 
 #include "decider_model.h"
@@ -52,9 +53,13 @@ void pick_fg(int K, int F_hint, int *F, int *G) {
   *G = bestG;
 }
 
+// model feature idx: 0..15 = the Table-3 fields in header order, 16 =
+// log2(K), 17 = log2(n K 4 / L2 bytes) (B's footprint against the L2; the
+// signal of the single-pass guard, learned from the sweep since round 2)
 double feature_value(const pspmm_features *f, int idx, int K) {
   const double *v = reinterpret_cast<const double *>(f);
   if (idx >= 0 && idx < 16) return v[idx];
+  if (idx == 17) return std::log2(std::max(f->n, 1.0) * (double)K * 4.0 / kL2Bytes);
   return std::log2((double)K);
 }
 

@@ -11,13 +11,17 @@
 // lo = rna(x - hi); X.W ~ Xhi.Whi + Xhi.Wlo + Xlo.Whi (the dropped lo.lo
 // term is below 2^-22 relative), accumulated in fp32 in TMEM.
 //
-// One persistent CTA per SM, warp-specialised (9 warps):
-//  - warps 0-3 (loaders): thread r owns row r of the current 128-row tile;
-//    per 32-column chunk of X it loads its 128 contiguous bytes (8 x LDG.128),
-//    splits them and writes hi / lo into a stage in the no-swizzle K-major
+// One persistent CTA per SM, warp-specialised (10 warps):
+//  - warp 9 lane 0 (TMA): streams X in chunks of 128 rows x 32 columns
+//    (16 KB, one 2-D TMA copy, 128-B swizzle, rows past n zero-filled) into
+//    a ring of up to 8 raw stages, so up to 128 KB of X is in flight per SM
+//    (thread-issued loads kept only 16 KB in flight: 1.8 TB/s);
+//  - warps 0-3 (splitters): thread r owns row r of the chunk; it reads its
+//    128 bytes from the raw stage (swizzled, conflict-free), splits them and
+//    writes hi / lo into an operand stage in the no-swizzle K-major
 //    core-matrix layout (core matrix = 8 rows x 16 B; consecutive rows 16 B
 //    apart, so the stores are conflict-free), then fence.proxy.async and an
-//    mbarrier arrive; `stages` chunks in flight;
+//    mbarrier arrive;
 //  - warp 4 lane 0 (MMA): per chunk 4 K-steps x 3 tcgen05.mma.kind::tf32
 //    (M = 128, N = Ko, K = 8) into one of two TMEM accumulators (2 x Ko
 //    columns), tcgen05.commit frees the stage / publishes the accumulator;
@@ -26,6 +30,9 @@
 //    free the accumulator, so the next tile's MMAs overlap this epilogue.
 //  W's hi / lo image (all of Ki x Ko) is split once per CTA into shared
 //  memory by the loaders before the first tile.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -37,8 +44,10 @@ constexpr int kM = 128;                 // rows per tile (MMA M, TMEM lanes)
 constexpr int kKc = 32;                 // X columns per chunk
 constexpr int kChunkPart = kM * kKc * 4;  // one part (hi or lo) of a chunk: 16 KB
 constexpr int kChunkBytes = 2 * kChunkPart;
+constexpr int kRawBytes = kM * kKc * 4;  // one raw fp32 chunk: 16 KB
 constexpr int kLoaders = 128, kEpi = 128;
-constexpr int kThreads = kLoaders + 32 + kEpi;  // 288
+constexpr int kThreads = kLoaders + 32 + kEpi + 32;  // 320: splitters, MMA, epilogue, TMA
+constexpr int kOpStages = 2;
 constexpr int kMaxSmem = 227 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -108,25 +117,42 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                       int r0) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(r0)
+      : "memory");
+}
+
 struct GemmArgs {
   const float *__restrict__ X;
   const float *__restrict__ W;
   float *__restrict__ T;
   int64_t n, ldx, ldw, ldt;
-  int32_t Ki, Ko, stages, tmem_cols;
+  int32_t Ki, Ko, raw_stages, tmem_cols;
 };
 
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) {
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-  const int Ki = a.Ki, Ko = a.Ko, S = a.stages;
+  const int Ki = a.Ki, Ko = a.Ko, S = kOpStages, R = a.raw_stages;
   const uint32_t wpart = (uint32_t)Ki * Ko * 4;  // one part of W's image
-  uint8_t *wimg = smem;                          // [hi | lo], each [Ki/4][Ko][4]
-  uint8_t *stage0 = smem + 2 * wpart;            // S x [hi 16 KB | lo 16 KB]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(stage0 + (size_t)S * kChunkBytes);
+  uint8_t *raw0 = smem;                          // R x 16 KB raw X chunks (1 KB aligned)
+  uint8_t *stage0 = raw0 + (size_t)R * kRawBytes;  // S x [hi 16 KB | lo 16 KB]
+  uint8_t *wimg = stage0 + (size_t)S * kChunkBytes;  // [hi | lo], each [Ki/4][Ko][4]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(wimg + 2 * wpart);
   uint64_t *full = bar, *empty = bar + S, *accf = bar + 2 * S, *acce = bar + 2 * S + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 2 * S + 4);
+  uint64_t *rfull = bar + 2 * S + 4, *rempty = rfull + R;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + R);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t tiles = (a.n + kM - 1) / kM;
   const int chunks = Ki / kKc;
@@ -145,6 +171,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], kEpi);
+    }
+    for (int r = 0; r < R; ++r) {
+      mbar_init(&rfull[r], 1);
+      mbar_init(&rempty[r], kLoaders);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -171,20 +201,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {  // loaders: thread tid owns row tid of each tile
-    int it = 0;    // chunk counter across tiles (stage ring position)
+  if (warp == 9) {  // TMA producer: raw X chunks
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x)
+        for (int c = 0; c < chunks; ++c, ++it) {
+          const int r = it % R;
+          if (it >= R) mbar_wait(&rempty[r], ((it / R) - 1) & 1);
+          mbar_expect_tx(&rfull[r], kRawBytes);
+          tma_2d(smem_u32(raw0 + (size_t)r * kRawBytes), &xmap, &rfull[r], c * kKc, (int)(t * kM));
+        }
+    }
+    __syncwarp();
+  } else if (warp < 4) {  // splitters: thread tid owns row tid of each chunk
+    int it = 0;           // chunk counter across tiles (both rings advance together)
+    const uint32_t sw = (uint32_t)(tid & 7);
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int64_t row = t * kM + tid;
-      const float *xr = a.X + row * a.ldx;
       for (int c = 0; c < chunks; ++c, ++it) {
-        const int s = it % S;
-        if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
-        uint8_t *st = stage0 + (size_t)s * kChunkBytes;
+        const int r = it % R, s = it % S;
+        mbar_wait(&rfull[r], (it / R) & 1);
+        const uint8_t *rw = raw0 + (size_t)r * kRawBytes + tid * 128;
         float4 x[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-          x[g] = row < a.n ? __ldcs(reinterpret_cast<const float4 *>(xr + c * kKc + 4 * g))
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int g = 0; g < 8; ++g)  // 128-B swizzle: chunk g of row i at g ^ (i % 8)
+          x[g] = *reinterpret_cast<const float4 *>(rw + ((g ^ sw) << 4));
+        mbar_arrive(&rempty[r]);
+        if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+        uint8_t *st = stage0 + (size_t)s * kChunkBytes;
 #pragma unroll
         for (int g = 0; g < 8; ++g) {  // core-matrix layout: [k-group][row][16 B]
           float4 hi, lo;
@@ -228,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const GemmArgs a) 
       }
     }
     __syncwarp();
-  } else {  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31
+  } else {  // epilogue (warps 5-8): warp w reads TMEM lanes 32 (w % 4) .. + 31
     const int quarter = warp & 3;
     int tl = 0;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
@@ -276,16 +319,31 @@ bool gemm_tc_supported(int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx, co
   if ((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_W) |
        reinterpret_cast<uintptr_t>(d_T)) & 15)
     return false;
+  if (!tensor_map_encoder()) return false;
   const int64_t w = 2ll * Ki * Ko * 4;
-  return w + 2ll * kChunkBytes + 1024 + 256 <= kMaxSmem;
+  return w + (int64_t)kOpStages * kChunkBytes + 2ll * kRawBytes + 1024 + 512 <= kMaxSmem;
 }
 
 pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
                      const float *d_W, int64_t ldw, float *d_T, int64_t ldt, cudaStream_t stream) {
   if (n == 0) return PSPMM_OK;
+  if (n > 0x7fffffffll) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "dense_gemm: n >= 2^31");
   const int64_t w = 2ll * Ki * Ko * 4;
-  const int stages = (int)std::min<int64_t>(4, (kMaxSmem - 1024 - 256 - w) / kChunkBytes);
-  const size_t smem = (size_t)(w + (int64_t)stages * kChunkBytes + 1024 + 256);
+  const int raw = (int)std::min<int64_t>(
+      8, (kMaxSmem - 1024 - 512 - w - (int64_t)kOpStages * kChunkBytes) / kRawBytes);
+  const size_t smem =
+      (size_t)(w + (int64_t)kOpStages * kChunkBytes + (int64_t)raw * kRawBytes + 1024 + 512);
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+  if (!encode) PSPMM_FAIL(PSPMM_ERR_CUDA, "dense_gemm: cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)Ki, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kKc, (cuuint32_t)kM};
+  cuuint32_t estr[2] = {1, 1};
+  if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(d_X), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    PSPMM_FAIL(PSPMM_ERR_CUDA, "dense_gemm: tensor map encode failed");
   PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   GemmArgs args;
@@ -298,11 +356,11 @@ pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_
   args.ldt = ldt;
   args.Ki = Ki;
   args.Ko = Ko;
-  args.stages = stages;
+  args.raw_stages = raw;
   args.tmem_cols = tmem_cols_for(Ko);
   const int64_t tiles = (n + kM - 1) / kM;
   const int grid = (int)std::min<int64_t>(tiles, num_sms());
-  gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(args);
+  gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(map, args);
   PSPMM_CUDA_TRY(cudaGetLastError());
   return PSPMM_OK;
 }

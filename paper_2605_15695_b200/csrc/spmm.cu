@@ -218,12 +218,13 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
       PSPMM_FAIL(PSPMM_ERR_CONFIG_MISMATCH, "spmm_run: cfg.V/S/omega differ from the PCSR handle");
     return run_spmm_dense(A, d_B, ldb, K, d_C, ldc, cfg, stream, accumulate);
   }
-  if (cfg.mode == 5) {  // row blocks with shared-memory B reuse (spmm_block.cu)
+  if (cfg.mode == 5 || cfg.mode == 6) {  // row blocks / staged bands (spmm_block.cu, spmm_band.cu)
     if (!A || !d_B || !d_C) PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run: null handle or pointer");
     if (K < 1 || ldb < K || ldc < K)
       PSPMM_FAIL(PSPMM_ERR_DIM_MISMATCH, "spmm_run: need K >= 1, ldb >= K, ldc >= K");
     if (cfg.V != A->V || cfg.S != A->S || cfg.omega != A->omega)
       PSPMM_FAIL(PSPMM_ERR_CONFIG_MISMATCH, "spmm_run: cfg.V/S/omega differ from the PCSR handle");
+    if (cfg.mode == 6) return run_spmm_band(A, d_B, ldb, K, d_C, ldc, stream, accumulate, f);
     return run_spmm_block(A, d_B, ldb, K, d_C, ldc, stream, accumulate, f);
   }
   Plan plan;
@@ -257,7 +258,7 @@ pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32
                            cudaStream_t stream) {
   if (!A || !h_B || !h_C)
     PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_host: null handle or host pointer");
-  if (cfg.mode == 1 || cfg.mode == 5) {  // one whole-matrix product, no slices
+  if (cfg.mode == 1 || cfg.mode == 5 || cfg.mode == 6) {  // one whole-matrix product, no slices
     PSPMM_CUDA_TRY(cudaMemcpyAsync(d_Bbuf, h_B, (size_t)A->n_cols * ldb * sizeof(float),
                                    cudaMemcpyHostToDevice, stream));
     pspmm_status st = run_spmm(A, d_Bbuf, ldb, K, d_Cbuf, ldc, cfg, stream);
@@ -317,7 +318,7 @@ pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64
                                  const pspmm_config &cfg, float *const *d_B, float *const *d_C,
                                  cudaStream_t stream) {
   Plan plan[2];
-  for (int b = 0; b < 2 && cfg.mode != 1 && cfg.mode != 5; ++b) {
+  for (int b = 0; b < 2 && cfg.mode != 1 && cfg.mode != 5 && cfg.mode != 6; ++b) {
     pspmm_status st = make_plan(A, d_B[b], ldb, K, d_C[b], ldc, cfg, &plan[b]);
     if (st != PSPMM_OK) return st;
   }
@@ -348,7 +349,7 @@ pspmm_status run_spmm_host_batch(pspmm_pcsr_s *A, const float *const *h_B, int64
     PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->h2d_done[b], 0));
     if (i >= 2) PSPMM_CUDA_TRY(cudaStreamWaitEvent(stream, A->d2h_done[b], 0));
     pspmm_status st;
-    if (cfg.mode == 1 || cfg.mode == 5) {  // whole-matrix modes (validate their own arguments)
+    if (cfg.mode == 1 || cfg.mode == 5 || cfg.mode == 6) {  // whole-matrix modes
       st = run_spmm(A, d_B[b], ldb, K, d_C[b], ldc, cfg, stream);
     } else {
       st = prepare_c(A, K, d_C[b], ldc, stream, none);

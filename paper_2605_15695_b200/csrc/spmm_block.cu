@@ -309,7 +309,7 @@ __global__ void touched_windows_kernel(const int32_t *__restrict__ rowptr,
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(total, c);
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_impl() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -332,6 +332,9 @@ pspmm_status upload(T **dst, const std::vector<T> &src) {
 }
 
 }  // namespace
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+void *tensor_map_encoder() { return reinterpret_cast<void *>(get_encode_impl()); }
 
 void destroy_blocks(RowBlocks *B) {
   if (!B) return;
@@ -605,7 +608,7 @@ pspmm_status run_spmm_block(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb
   if (R->num_blocks == 0) return PSPMM_OK;
   if (K / kKs > 65535 || R->num_blocks * (K / kKs) > 0x7fffffff)
     PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run mode 5: grid too large");
-  auto encode = get_encode();
+  auto encode = get_encode_impl();
   if (!encode) PSPMM_FAIL(PSPMM_ERR_CUDA, "spmm_run mode 5: cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)std::max<int64_t>(1, A->n_cols)};
