@@ -299,6 +299,9 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
     # engine mode 5 (row blocks, B windows staged in shared memory): taken
     # when each staged B row would serve enough nonzeros (device-measured)
     cfg, A, blocks = api.auto_blocks(A, rp, ci, vl, K, cfg, stream)
+    # engine mode 6 (staged bands): locality-ordered graphs whose 128-row
+    # blocks' B-row ranges fit the shared-memory budget
+    cfg, A, band = api.auto_band(A, rp, ci, vl, K, cfg, feats, stream)
     t3 = time.perf_counter()
     B = gen.config_B(g.name, g.n)
     Bd = torch.from_numpy(B).cuda()
@@ -316,9 +319,10 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
     # steady state of an iterative GNN), median, beside the cold mean above
     tw = time_steps(step, max(steps, 20), 2, lambda: None, stream)
     mode0 = None
-    if cfg.mode in (1, 5):  # the decider's mode-0 pick alone, for comparison
+    if cfg.mode in (1, 5, 6):  # the decider's own pick alone, for comparison
         c0 = api.Config(**(cfg.as_dict() if cfg.mode == 1 else cfg0.as_dict()))
-        c0.mode = 0
+        if cfg.mode == 1:
+            c0.mode = 0
         A0 = A if cfg.mode == 1 else A_dec
         t0s = time_steps(lambda: A0.run(Bd, C, c0, stream), steps, warmup, flush, stream)
         mode0 = {"cfg": c0.as_dict(), "ms_median": float(np.median(t0s)),
@@ -340,6 +344,8 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
         out["dense_split"] = dense
     if blocks is not None:
         out["row_blocks"] = blocks
+    if band is not None:
+        out["staged_band"] = band
     if mode0 is not None:
         out["mode0_same_knobs"] = mode0
     if want_cusparse:
@@ -413,7 +419,7 @@ def main():
                     help="N>1: all-gather then SpMM, instead of overlapping the all-gather "
                          "with the own-column block")
     ap.add_argument("--exchange", default="auto",
-                    choices=["auto", "allgather", "halo", "fanout"],
+                    choices=["auto", "allgather", "halo", "fanout", "multicast"],
                     help="N>1: row exchange (auto: halo when every rank references < 50 %% "
                          "of the remote rows, else the all-gather fused into the SpMM "
                          "epilogue (fanout) when the peers map over CUDA IPC, else the "
@@ -623,7 +629,7 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
     elif frac < 0.5:
         legs = ["halo", "allgather"]
     else:
-        legs = ["allgather", "fanout"]
+        legs = ["allgather", "fanout", "multicast"]
 
     def launches(h):  # engine kernel + the split-panel zeroing kernel when present
         return 1 + (1 if (h.info["S"] == 1 and h.info["num_chunks"] > h.info["num_panels"])
@@ -632,10 +638,10 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
     def setup(kind):
         """-> dict(step, kernel_only, e2e_body, lo, rows, n_cols, nnz_loc, launches,
         desc, moved) or a string saying why the leg is unavailable."""
-        if kind == "fanout":
-            run, note = setup_fanout(g, cfg, B, world, rank, stream)
+        if kind in ("fanout", "multicast"):
+            run, note = setup_fanout(g, cfg, B, world, rank, stream, kind == "multicast")
             if run is None:
-                return note or "fanout unavailable"
+                return note or f"{kind} unavailable"
             sh = run.shard
             split = run.A.info["S"] == 1 and run.A.info["num_chunks"] > run.A.info["num_panels"]
             C_k = torch.empty((sh.rows, K), device="cuda")
@@ -652,9 +658,13 @@ def run_sharded(g, args, world, rank, stream, flush, sampler):
                 e2e_body=e2e_body, lo=sh.lo, rows=sh.rows, n_cols=sh.n_cols,
                 nnz_loc=int(sh.rowptr[-1]), launches=1 + (world if split else 0),
                 moved=(world - 1) * sh.rows * K * 4, keep=run,
-                desc="pspmm_spmm_run_fanout: SpMM whose epilogue stores each output row into "
-                     "every rank's next-layer B (CUDA-IPC peer memory over NVLink), then a "
-                     "one-element NCCL all-reduce as the layer barrier; no separate collective")
+                desc=("pspmm_spmm_run_multicast: SpMM whose epilogue writes each output element "
+                      "ONCE with multimem.st to an NVSwitch multicast object binding every "
+                      "rank's next-layer B (torch symmetric memory), then a one-element NCCL "
+                      "all-reduce as the layer barrier" if kind == "multicast" else
+                      "pspmm_spmm_run_fanout: SpMM whose epilogue stores each output row into "
+                      "every rank's next-layer B (CUDA-IPC peer memory over NVLink), then a "
+                      "one-element NCCL all-reduce as the layer barrier; no separate collective"))
         if kind == "halo":
             plan = pdist.make_halo_plan(g.rowptr, g.colidx, g.val, world, rank)
             with torch.cuda.stream(stream):
@@ -751,10 +761,12 @@ EXCHANGE_DESC = {
     "allgather": "all-gather of B rows (NCCL)",
     "fanout": "all-gather fused into the SpMM epilogue (P2P stores to every rank's next-layer "
               "B over CUDA IPC / NVLink)",
+    "multicast": "all-gather fused into the SpMM epilogue as NVLS multimem stores (one store "
+                 "per element, replicated by the NVSwitch)",
 }
 
 
-def setup_fanout(g, cfg, B, world, rank, stream):
+def setup_fanout(g, cfg, B, world, rank, stream, multicast=False):
     """Map every peer's gathered buffers (CUDA IPC) and validate one fused
     step against the plain engine on the same gathered input on all ranks.
     Returns (FanoutSpmm or None, note); every rank reaches the same decision
@@ -763,7 +775,7 @@ def setup_fanout(g, cfg, B, world, rank, stream):
     from paper_2605_15695_b200 import api, dist as pdist
     sh = pdist.make_shard(g.rowptr, g.colidx, g.val, world, rank, align=2)
     with torch.cuda.stream(stream):
-        run = pdist.FanoutSpmm(sh, g.K, cfg, stream=stream)
+        run = (pdist.MulticastSpmm if multicast else pdist.FanoutSpmm)(sh, g.K, cfg, stream=stream)
     torch.cuda.synchronize()
     err = ""
     try:

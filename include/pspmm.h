@@ -394,6 +394,26 @@ pspmm_status pspmm_spmm_run_fanout(pspmm_pcsr A, const float *d_B, int64_t ldb, 
                                    pspmm_config cfg, void *stream);
 
 /*
+ * (f2 (i) over NVLS: SURVEY §8(f) f2 "NVLS multicast (multimem.st via
+ * symmetric memory) fusing the allgather into the SpMM epilogue")
+ * C = A . B with every C write issued as ONE multimem store (split-panel
+ * atomics: one multimem reduction, their zeroing: multimem stores of 0) to
+ * d_C_mc, the multicast address of d_C: an address of an NVSwitch multicast
+ * object every rank's copy of the gathered next-layer buffer is bound to
+ * (e.g. torch.distributed._symmetric_memory's multicast_ptr plus d_C's
+ * offset in the buffer).  The switch delivers the value to every bound copy,
+ * d_C's own memory included, so no separate local store and no per-peer
+ * unicast stores are issued.  d_C is read only when the engine needs C's old
+ * value (never for C = A.B).  Engine modes 0, 3, 5 and 6 (mode 1, 2, 4:
+ * PSPMM_ERR_UNSUPPORTED); same fences and barrier contract as
+ * pspmm_spmm_run_fanout.  INVALID_ARG for a null d_C_mc or an alignment
+ * differing from d_C's.  Asynchronous.
+ */
+pspmm_status pspmm_spmm_run_multicast(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
+                                      float *d_C, int64_t ldc, float *d_C_mc, pspmm_config cfg,
+                                      void *stream);
+
+/*
  * CUDA IPC plumbing for the fan-out (f2): export a device allocation made
  * with cudaMalloc (or any sub-range of one, as caching allocators hand out) as a 64-byte
  * handle, open a peer process's handle (peer access enabled lazily) and

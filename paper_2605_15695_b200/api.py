@@ -121,6 +121,7 @@ _sig("pspmm_spmm_run_host_batch", _st, _P, _P, _i64, _i32, _P, _i64, _i32, Confi
 _sig("pspmm_dense_gemm", _st, _i64, _i32, _i32, _P, _i64, _P, _i64, _P, _i64, _P)
 _sig("pspmm_gnn_layer", _st, _P, _P, _i64, _i32, _P, _i64, _i32, _P, _i64, _P, _i64, Config, _P)
 _sig("pspmm_spmm_run_fanout", _st, _P, _P, _i64, _i32, _P, _i64, _P, _i32, Config, _P)
+_sig("pspmm_spmm_run_multicast", _st, _P, _P, _i64, _i32, _P, _i64, _P, Config, _P)
 _sig("pspmm_ipc_get_handle", _st, _P, _P, ctypes.POINTER(_i64))
 _sig("pspmm_ipc_open", _st, _P, ctypes.POINTER(_P))
 _sig("pspmm_ipc_close", _st, _P)
@@ -442,6 +443,18 @@ def pspmm_gnn_layer(A: Pcsr, X, W, T, Y, cfg: Config, stream=None):
 MAX_PEERS = 7  # PSPMM_MAX_PEERS
 
 
+def pspmm_spmm_run_multicast(A: Pcsr, B, C, c_mc: int, cfg: Config, stream=None):
+    """C = A . B with every C write issued once as a multimem store to c_mc,
+    the multicast address (int) of C's first element (f2 i over NVLS)."""
+    b, ldb = _dense(B, "B")
+    c, ldc = _dense(C, "C")
+    K = B.shape[1]
+    if B.shape[0] < A.n_cols or C.shape[0] < A.n_rows or C.shape[1] < K:
+        raise ValueError("B (n_cols x K) / C (n_rows x K) shapes do not match A")
+    _check(_lib.pspmm_spmm_run_multicast(A.handle, b, ldb, K, c, ldc, ctypes.c_void_p(int(c_mc)),
+                                         cfg, _stream(stream)), "pspmm_spmm_run_multicast")
+
+
 def pspmm_spmm_run_fanout(A: Pcsr, B, C, peers, cfg: Config, stream=None, K=None):
     """C = A . B with every written C element also stored at the same offset
     of each peer buffer (f2).  peers: device addresses (int, e.g. from
@@ -677,6 +690,36 @@ def auto_blocks(A: Pcsr, rowptr, colidx, val, K, cfg: Config, stream=None):
     c = pspmm_decide_blocks(H, K, BLOCK_MIN_REUSE, c)
     info["taken"] = c.mode == 5
     return (c, H, info) if c.mode == 5 else (cfg, A, info)
+
+
+# engine mode 6 rule: locality-ordered graphs (mean row
+# bandwidth below n / BAND_MAX_B_FRAC) whose 128-row blocks' bands fit the
+# shared-memory budget for >= BAND_MIN_STAGED of the blocks
+BAND_MAX_B_FRAC = 64.0
+BAND_MIN_STAGED = 0.9
+
+
+def auto_band(A: Pcsr, rowptr, colidx, val, K, cfg: Config, features=None, stream=None):
+    """Engine mode 6 (staged bands) for locality-ordered graphs, K % 4 == 0,
+    K <= 128, when the decider's pick is a CUDA-core gather engine: returns
+    (cfg, handle to run, info or None)."""
+    if K % 4 != 0 or K > 128 or cfg.mode in (1, 5):
+        return cfg, A, None
+    f = features if features is not None else pspmm_features_compute(
+        A.n_rows, int(colidx.shape[0]), rowptr, colidx, stream=stream)
+    b = f["b"] if isinstance(f, dict) else f.b
+    info = {"b": b, "max_b": A.n_rows / BAND_MAX_B_FRAC, "taken": False}
+    if not b < A.n_rows / BAND_MAX_B_FRAC:
+        return cfg, A, info
+    H = A
+    if not (A.V == 1 and A.info["S"] == 0):
+        H = pspmm_pcsr_build(A.n_rows, int(colidx.shape[0]), rowptr, colidx, val, 1, 0,
+                             stream=stream, n_cols=A.n_cols)
+    info["staged_frac"] = pspmm_pcsr_attach_band(H, K, stream)
+    if info["staged_frac"] < BAND_MIN_STAGED:
+        return cfg, A, info
+    info["taken"] = True
+    return Config(V=1, S=0, mode=6), H, info
 
 
 def spmm(rowptr, colidx, val, B, cfg: Config | None = None, stream=None, C=None):

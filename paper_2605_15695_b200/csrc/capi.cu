@@ -229,6 +229,26 @@ pspmm_status pspmm_spmm_run_fanout(pspmm_pcsr A, const float *d_B, int64_t ldb, 
   });
 }
 
+pspmm_status pspmm_spmm_run_multicast(pspmm_pcsr A, const float *d_B, int64_t ldb, int32_t K,
+                                      float *d_C, int64_t ldc, float *d_C_mc, pspmm_config cfg,
+                                      void *stream) {
+  return pspmm::guarded("spmm_run_multicast", [&]() -> pspmm_status {
+    if (!d_C_mc) {
+      set_error("spmm_run_multicast: null multicast address");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    if ((reinterpret_cast<uintptr_t>(d_C_mc) & 15) != (reinterpret_cast<uintptr_t>(d_C) & 15)) {
+      set_error("spmm_run_multicast: multicast address alignment differs from C's");
+      return PSPMM_ERR_INVALID_ARG;
+    }
+    Fanout fan{};
+    fan.n = 1;
+    fan.mc = 1;
+    fan.peer[0] = d_C_mc;
+    return run_spmm(A, d_B, ldb, K, d_C, ldc, cfg, as_stream(stream), 0, &fan);
+  });
+}
+
 pspmm_status pspmm_ipc_get_handle(const void *d_ptr, void *h_handle, int64_t *offset) {
   return pspmm::guarded("ipc_get_handle", [&]() -> pspmm_status {
     if (!d_ptr || !h_handle || !offset) {

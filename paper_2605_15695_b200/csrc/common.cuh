@@ -162,7 +162,43 @@ constexpr int kMaxPeers = PSPMM_MAX_PEERS;
 struct Fanout {
   float *peer[kMaxPeers];
   int32_t n;
+  // mc = 1 (NVLS, f2 i): peer[0] is the multicast address of C (NVLink
+  // SHARP / NVSwitch multicast object every rank's copy is bound to) and
+  // n = 1: each C write is ONE multimem store (or reduction) that the switch
+  // delivers to every bound copy, the local one included, instead of the
+  // local write plus n unicast peer stores.
+  int32_t mc;
 };
+#ifdef __CUDACC__
+__device__ __forceinline__ void mc_st(float *p, const float4 &v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mc_st(float *p, const float &v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void mc_red(float *p, const float4 &v) {
+  asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mc_red(float *p, const float &v) {
+  asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+// The store epilogue of the row-owning engines (modes 3, 5, 6): C[off] = v
+// (v already includes C's old value when accumulating), fanned out.
+__device__ __forceinline__ void fan_store4(float *C, const Fanout &fan, int64_t off,
+                                           const float4 &v) {
+  if (fan.mc) {
+    mc_st(fan.peer[0] + off, v);
+    return;
+  }
+  __stcs(reinterpret_cast<float4 *>(C + off), v);
+#pragma unroll 1
+  for (int d = 0; d < fan.n; ++d) __stcs(reinterpret_cast<float4 *>(fan.peer[d] + off), v);
+}
+#endif
 
 // spmm_dense.cu (engine mode 1)
 bool dense_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc, const float *d_B,

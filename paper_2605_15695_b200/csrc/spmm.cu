@@ -10,24 +10,37 @@ namespace {
 using namespace detail;
 
 // Zero the C rows of panels that own more than one chunk (S = 1, c-12).
+// mc = 1: C is a multicast address, zeroed with multimem stores (every
+// bound copy at once).
 __global__ void zero_split_kernel(const int32_t *__restrict__ split, int64_t num_split, int V,
-                                  int64_t n_rows, int32_t K, float *__restrict__ C, int64_t ldc) {
+                                  int64_t n_rows, int32_t K, float *__restrict__ C, int64_t ldc,
+                                  int mc) {
   const int64_t per = (int64_t)V * K;
   const int64_t total = num_split * per;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = t / per, r = t % per;
     const int64_t row = (int64_t)split[s] * V + r / K;
-    if (row < n_rows) C[row * ldc + r % K] = 0.f;
+    if (row < n_rows) {
+      if (mc)
+        mc_st(C + row * ldc + r % K, 0.f);
+      else
+        C[row * ldc + r % K] = 0.f;
+    }
   }
 }
 
 // C = 0 (nnz_V == 0).
-__global__ void zero_all_kernel(int64_t n_rows, int32_t K, float *__restrict__ C, int64_t ldc) {
+__global__ void zero_all_kernel(int64_t n_rows, int32_t K, float *__restrict__ C, int64_t ldc,
+                                int mc) {
   const int64_t total = n_rows * K;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x)
-    C[(t / K) * ldc + t % K] = 0.f;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (mc)
+      mc_st(C + (t / K) * ldc + t % K, 0.f);
+    else
+      C[(t / K) * ldc + t % K] = 0.f;
+  }
 }
 
 KernelFn pick_kernel(int V, int S, bool vec, int F, int G, bool na) {
@@ -130,18 +143,19 @@ pspmm_status make_plan(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int
 // With a fan-out the peer copies are zeroed the same way.
 pspmm_status prepare_c(const pspmm_pcsr_s *A, int32_t K, float *d_C, int64_t ldc,
                        cudaStream_t stream, const Fanout &fan) {
-  for (int d = -1; d < fan.n; ++d) {
+  for (int d = fan.mc ? 0 : -1; d < fan.n; ++d) {  // multicast: the one mc address
     float *C = d < 0 ? d_C : fan.peer[d];
     if (A->nnz_v == 0) {
       const int64_t total = A->n_rows * K;
       const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
-      zero_all_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(A->n_rows, K, C, ldc);
+      zero_all_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(A->n_rows, K, C, ldc,
+                                                                    fan.mc);
       PSPMM_CUDA_TRY(cudaGetLastError());
     } else if (A->S == 1 && A->num_split > 0) {
       const int64_t total = A->num_split * A->V * (int64_t)K;
       const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
       zero_split_kernel<<<blocks, 256, 0, stream>>>(A->d_split, A->num_split, A->V, A->n_rows,
-                                                     K, C, ldc);
+                                                     K, C, ldc, fan.mc);
       PSPMM_CUDA_TRY(cudaGetLastError());
     }
   }
@@ -210,6 +224,11 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
           (reinterpret_cast<uintptr_t>(d_C) & 15))
         PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_fanout: peer alignment differs from C's");
     }
+    if (fan->mc && fan->n != 1)
+      PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_multicast: exactly one multicast address");
+    if (fan->mc && (cfg.mode == 2 || cfg.mode == 4))
+      PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
+                 "spmm_run_multicast: engine modes 0, 3, 5 and 6 take the multicast epilogue");
     f = *fan;
   }
   if (cfg.mode == 1) {  // dense tiles on the tensor cores + the rest (spmm_dense.cu)

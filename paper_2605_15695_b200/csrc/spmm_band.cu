@@ -187,10 +187,7 @@ __global__ void __launch_bounds__(kThreads, 3) spmm_band_kernel(const BandArgs a
         acc.z += o.z;
         acc.w += o.w;
       }
-      __stcs(p, acc);
-#pragma unroll 1
-      for (int d = 0; d < a.fan.n; ++d)
-        __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + off), acc);
+      fan_store4(a.C, a.fan, off, acc);
     }
   }
   if (a.fan.n) __threadfence_system();

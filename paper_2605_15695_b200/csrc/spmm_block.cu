@@ -280,9 +280,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
       v.z += o.z;
       v.w += o.w;
     }
-    __stcs(p, v);
-#pragma unroll 1
-    for (int d = 0; d < a.fan.n; ++d) __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + off), v);
+    fan_store4(a.C, a.fan, off, v);
   }
   if (a.fan.n) __threadfence_system();
 }

@@ -122,6 +122,10 @@ __device__ __forceinline__ void st_c(float *p, float v, int accumulate = 0) {
   if (accumulate) v += *p;
   __stcs(p, v);
 }
+__device__ __forceinline__ float4 add_c(const float4 &o, const float4 &v) {
+  return make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+}
+__device__ __forceinline__ float add_c(const float &o, const float &v) { return o + v; }
 __device__ __forceinline__ void red_c(float4 *p, const float4 &v) { atomicAdd(p, v); }
 __device__ __forceinline__ void red_c(float *p, const float &v) { atomicAdd(p, v); }
 
@@ -131,6 +135,16 @@ __device__ __forceinline__ void red_c(float *p, const float &v) { atomicAdd(p, v
 template <typename T>
 __device__ __forceinline__ void put_c(const SpmmArgs &a, int64_t off, const T &v, bool red) {
   T *p = reinterpret_cast<T *>(a.C + off);
+  if (a.fan.mc) {  // NVLS: one multimem op reaches every bound copy (local included)
+    if (red) {
+      mc_red(a.fan.peer[0] + off, v);
+    } else {
+      T w = v;
+      if (a.accumulate) w = add_c(*p, w);
+      mc_st(a.fan.peer[0] + off, w);
+    }
+    return;
+  }
   if (red)
     red_c(p, v);
   else

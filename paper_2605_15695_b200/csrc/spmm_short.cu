@@ -161,12 +161,7 @@ __global__ void __launch_bounds__(256, PSPMM_SHORT_MINB) spmm_short_kernel(const
           v.z += o.z;
           v.w += o.w;
         }
-        __stcs(crow + f * G, v);
-#pragma unroll 1
-        for (int d = 0; d < a.fan.n; ++d)
-          __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + (int64_t)r * a.ldc + col0 + l * 4) +
-                     f * G,
-                 v);
+        fan_store4(a.C, a.fan, (int64_t)r * a.ldc + col0 + l * 4 + f * G * 4, v);
       }
     h0 = h1;
     t0 = t1;
@@ -314,12 +309,7 @@ __global__ void __launch_bounds__(256) spmm_ring_kernel(const ShortArgs a) {
           v.z += o.z;
           v.w += o.w;
         }
-        __stcs(crow + f * G, v);
-#pragma unroll 1
-        for (int d = 0; d < a.fan.n; ++d)
-          __stcs(reinterpret_cast<float4 *>(a.fan.peer[d] + (int64_t)r * a.ldc + col0 + l * 4) +
-                     f * G,
-                 v);
+        fan_store4(a.C, a.fan, (int64_t)r * a.ldc + col0 + l * 4 + f * G * 4, v);
       }
     h0 = h1; t0 = t1; c0 = c1; v0 = v1;
     h1 = h2; t1 = t2; c1 = c2; v1 = v2;

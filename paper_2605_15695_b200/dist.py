@@ -254,6 +254,55 @@ class FanoutSpmm:
         self.peers = [[], []]
 
 
+class MulticastSpmm(FanoutSpmm):
+    """f2 (i) over NVLS: the fan-out of FanoutSpmm with ONE multimem store per
+    C write.  The two gathered buffers live in one symmetric-memory
+    allocation (torch.distributed._symmetric_memory) whose NVSwitch
+    multicast object binds every rank's copy; the engine
+    (pspmm_spmm_run_multicast) writes each output element once to the
+    multicast address of slot `rank` and the switch replicates it into every
+    rank's buffer (the rank's own included).  connect() raises if the group
+    has no multicast support (the caller falls back to FanoutSpmm)."""
+
+    def __init__(self, shard: Shard, K: int, cfg: api.Config | None = None, device="cuda",
+                 stream=None):
+        super().__init__(shard, K, cfg, device, stream)
+        self._mc = None
+
+    def connect(self, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        g = group if group is not None else dist.group.WORLD
+        XX = symm_mem.empty((2, self.shard.n_cols, self.K), dtype=self.XX.dtype,
+                            device=self.XX.device)
+        XX.zero_()
+        hdl = symm_mem.rendezvous(XX, g.group_name)
+        mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+        if not mc:
+            raise RuntimeError("MulticastSpmm: no NVSwitch multicast for this group")
+        self._hdl = hdl
+        self.XX = XX
+        self.X = [XX[0], XX[1]]
+        buf_bytes = self.shard.n_cols * self.K * 4
+        self._mc = [mc + b * buf_bytes + self.slot_bytes for b in (0, 1)]
+
+    def connect_local(self, others):
+        raise NotImplementedError("MulticastSpmm needs a multicast object (connect)")
+
+    def step(self, stream=None, group=None, swap=True, barrier=True):
+        src, dst = self.cur, 1 - self.cur
+        out = self.own(dst)
+        api.pspmm_spmm_run_multicast(self.A, self.X[src], out, self._mc[dst], self.cfg, stream)
+        if swap:
+            self.cur = dst
+        if barrier:
+            self.barrier(group)
+        return out
+
+    def close(self):
+        self._mc = None
+
+
 def split_own_columns(shard: Shard):
     """Local CSR split into (own, remote) column blocks, both canonical:
     own = columns owned by this rank, remapped to local row indices of B

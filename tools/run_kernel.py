@@ -37,6 +37,8 @@ def main():
     A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, cfg.V, cfg.S, cfg.omega, cfg.sg_override)
     if cfg.mode == 5:
         print("blocks: windows", api.pspmm_pcsr_attach_blocks(A))
+    if cfg.mode == 6:
+        print("band: staged fraction", api.pspmm_pcsr_attach_band(A, g.K))
     if a.dense > 0:
         print(api.pspmm_pcsr_attach_dense(A, rp, ci, vl, a.dense, k_max=g.K))
         cfg.mode = 1
