@@ -57,22 +57,21 @@ struct RowBlocks {
   int2 *d_pairs = nullptr;         // (column - window start, value bits), windows padded to even
   int16_t *d_rowmap = nullptr;     // num_blocks x nw x rw: local row of a slot, -1 = none
 };
-// Engine mode 6 (spmm_band.cu): rows in blocks of kBandRows; per block the
-// contiguous ranges of B rows it touches (staged by bulk copies) and every
-// nonzero's slot in that band, attached by pspmm_pcsr_attach_band.  Derived
-// data, not part of the PCSR contract.
-constexpr int kBandRows = 128;
-constexpr int kBandBytes = 64 * 1024;  // staged band budget per block (3 CTAs per SM)
+// Engine mode 6 (spmm_band.cu): rows in blocks of 64 / 32 / 16 (by k_max);
+// per block a descriptor, the contiguous ranges of B rows it touches (staged
+// by bulk copies) and every nonzero's (band slot, value) pair, attached by
+// pspmm_pcsr_attach_band.  Derived data, not part of the PCSR contract.
+constexpr int kBandBytes = 32 * 1024;  // staged band budget per block (6 CTAs per SM)
 constexpr int kBandMaxK = 128;
 struct Band {
   int64_t num_blocks = 0;
-  int32_t k_max = 0;
+  int32_t k_max = 0, rows = 0;      // rows per block
   double staged_frac = 0.0;         // non-empty blocks whose band fits the budget
-  int32_t *d_slot = nullptr;        // nnz: band slot (staged block) or column (unstaged)
-  int32_t *d_rng_ptr = nullptr;     // num_blocks + 1
-  int32_t *d_rng_lo = nullptr;      // first B row of each range
-  int32_t *d_rng_len = nullptr;     // rows of each range
-  int32_t *d_blk_rows = nullptr;    // num_blocks: staged rows (-1 over budget, 0 empty)
+  int4 *d_desc = nullptr;           // num_blocks: {first range, ranges, p0, p1}
+  int32_t *d_staged = nullptr;      // num_blocks: staged rows (-1 over budget, 0 empty)
+  int4 *d_rng = nullptr;            // ranges: {first B row, rows, band slot, 0}
+  int2 *d_pairs = nullptr;          // nnz + 2: (band slot or column, value bits)
+  int32_t *d_rowptr = nullptr;      // n + 65: padded copy of rowPtr
 };
 struct pspmm_pcsr_s {
   int64_t n_rows = 0, n_cols = 0, num_panels = 0, nnz = 0, nnz_v = 0, num_chunks = 0;

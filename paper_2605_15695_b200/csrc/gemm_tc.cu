@@ -34,6 +34,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -225,6 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int g = 0; g < 8; ++g)  // 128-B swizzle: chunk g of row i at g ^ (i % 8)
           x[g] = *reinterpret_cast<const float4 *>(rw + ((g ^ sw) << 4));
+        // the raw stage is refilled by the TMA (async proxy) after this
+        // release: order the generic reads before it (WAR across proxies)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&rempty[r]);
         if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
         uint8_t *st = stage0 + (size_t)s * kChunkBytes;
@@ -329,8 +333,10 @@ pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_
   if (n == 0) return PSPMM_OK;
   if (n > 0x7fffffffll) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "dense_gemm: n >= 2^31");
   const int64_t w = 2ll * Ki * Ko * 4;
-  const int raw = (int)std::min<int64_t>(
+  int raw = (int)std::min<int64_t>(
       8, (kMaxSmem - 1024 - 512 - w - (int64_t)kOpStages * kChunkBytes) / kRawBytes);
+  if (const char *e = std::getenv("PSPMM_GEMM_RAW"))  // A/B knob for the tools (2..raw)
+    raw = std::max(2, std::min(raw, std::atoi(e)));
   const size_t smem =
       (size_t)(w + (int64_t)kOpStages * kChunkBytes + (int64_t)raw * kRawBytes + 1024 + 512);
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());

@@ -15,6 +15,9 @@ using namespace detail;
 __global__ void zero_split_kernel(const int32_t *__restrict__ split, int64_t num_split, int V,
                                   int64_t n_rows, int32_t K, float *__restrict__ C, int64_t ldc,
                                   int mc) {
+  // the engine (a programmatic dependent) may launch now; it waits for this
+  // grid's completion before its first write
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t per = (int64_t)V * K;
   const int64_t total = num_split * per;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -166,7 +169,7 @@ pspmm_status prepare_c(const pspmm_pcsr_s *A, int32_t K, float *d_C, int64_t ldc
 pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *d_B,
                           int64_t ldb, int32_t K, float *d_C, int64_t ldc,
                           const pspmm_config &cfg, cudaStream_t stream, int64_t u0, int64_t u1,
-                          int32_t accumulate, const Fanout &fan) {
+                          int32_t accumulate, const Fanout &fan, bool pdl = false) {
   if (A->nnz_v == 0 || u1 <= u0) return PSPMM_OK;
   if (cfg.mode == 2)
     return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate, fan);
@@ -201,6 +204,19 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
       std::min<int64_t>(32, (PSPMM_MAX_THREADS * PSPMM_MIN_BLOCKS) / plan.threads);
   if (PSPMM_WAVES > 0) bx = std::min<int64_t>(bx, (int64_t)num_sms() * resident * PSPMM_WAVES);
   if (bx > 0x7fffffff) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "spmm_run: grid too large");
+  if (pdl && A->S == 1) {  // overlap this launch with the zeroing kernel before it
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)bx, (unsigned)plan.by);
+    lc.blockDim = dim3(plan.threads);
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    PSPMM_CUDA_TRY(cudaLaunchKernelEx(&lc, plan.fn, args));
+    return PSPMM_OK;
+  }
   plan.fn<<<dim3((unsigned)bx, (unsigned)plan.by), plan.threads, 0, stream>>>(args);
   PSPMM_CUDA_TRY(cudaGetLastError());
   return PSPMM_OK;
@@ -253,8 +269,10 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
     st = prepare_c(A, K, d_C, ldc, stream, f);
     if (st != PSPMM_OK) return st;
   }
+  const bool zeroed = !accumulate && A->S == 1 && A->num_split > 0 && A->nnz_v > 0 &&
+                      cfg.mode == 0;
   return launch_range(A, plan, d_B, ldb, K, d_C, ldc, cfg, stream, 0, A->num_chunks, accumulate,
-                      f);
+                      f, zeroed);
 }
 
 namespace {

@@ -6,26 +6,31 @@
 // themselves and the rows one lattice width above and below).  The mode-0 /
 // mode-3 engines gather every B row with a dependent rowPtr -> colIdx ->
 // B-row chain per row, which keeps them latency-bound on such graphs
-// (roadNet: 58 % of the HBM roofline, long-scoreboard stalls).  Here the
-// chain is cut:
+// (roadNet: 58 % of the HBM roofline, long-scoreboard stalls).  Here every
+// byte a block needs moves by bulk copy, issued from one descriptor:
 //
-//  - pack (pspmm_pcsr_attach_band, once per graph): rows in blocks of
-//    kRows = 128; per block the sorted distinct columns merged into ranges
-//    (gaps of at most kGap rows are staged too), each range a contiguous run
-//    of B rows; every nonzero's column replaced by its row slot in the
-//    block's staged band (blocks whose band exceeds the budget keep the
-//    global column and gather from L2 / HBM instead);
-//  - kernel (one CTA of 256 threads per block, ~3 resident per SM): thread 0
-//    issues one 1-D bulk copy (cp.async.bulk, TMA engine) per range into
-//    shared memory; meanwhile every row group (G lanes = K / 4 columns, one
-//    float4 each) loads its rows' rowPtr pairs and (slot, value) pairs into
-//    registers (lane l holds nonzero l of the row); after the mbarrier
-//    completes, each nonzero is a warp-shuffle broadcast of (slot, value)
-//    and one LDS.128 of the staged B row (Alg. 2 l.9-15), and the row is
-//    written once with a streaming 128-bit store per lane (l.17-23).
+//  - pack (pspmm_pcsr_attach_band, once per graph): rows in blocks of R =
+//    64 / 32 / 16 rows (k_max <= 32 / 64 / 128, so the band of a lattice
+//    block fits the budget at any K); per block a descriptor {first range,
+//    ranges, first nonzero, end nonzero} and its staged-row count; per range
+//    {first B row, rows, slot in the band}, where a range is a run of the
+//    block's sorted distinct columns with gaps of at most kGap rows; per
+//    nonzero the pair (slot in the band, value bits), 8 B, in CSR order; a
+//    padded copy of rowPtr.  A block whose band exceeds kBandBytes keeps the
+//    global column in its pairs and gathers B from L2 / HBM;
+//  - kernel (persistent, 3 CTAs per SM, two stages each): a producer warp
+//    reads a block's descriptor, arms the stage's mbarrier with the total
+//    byte count and issues every copy at once, one range per lane
+//    (cp.async.bulk: the band's ranges, the block's pair run, its rowPtr
+//    slice), so the next block's data is in flight while four compute warps
+//    finish the current one; after the mbarrier completes, every row group
+//    (G lanes = K / 4 columns, one float4 each) walks its rows' pairs in
+//    shared memory: a
+//    broadcast LDS.64 of (slot, value) and one LDS.128 of the staged B row
+//    per nonzero (Alg. 2 l.9-15); one streaming 128-bit store per lane and
+//    row (l.17-23, one writer per element).
 //
-// The pack is derived data, not part of the bit-exact PCSR contract; the
-// handle's rowPtr and val are used as they are.
+// The pack is derived data, not part of the bit-exact PCSR contract.
 #include <algorithm>
 #include <cstring>
 #include <thread>
@@ -36,30 +41,38 @@
 namespace pspmm {
 namespace {
 
-constexpr int kRows = kBandRows;  // rows per block (CTA)
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kGap = 8;           // merge column ranges separated by <= kGap rows
+constexpr int kThreads = 128;
+constexpr int kGap = 8;              // merge column ranges separated by <= kGap rows
+constexpr int kPairCap = 512;        // pairs staged per block (4 KB); more: read from global
+
+int block_rows(int k_max) { return k_max <= 32 ? 64 : k_max <= 64 ? 32 : 16; }
 
 struct BandArgs {
-  const int32_t *__restrict__ rowptr;
-  const int32_t *__restrict__ slot;     // per nonzero: staged row slot, or global column
-  const float *__restrict__ val;
-  const int32_t *__restrict__ rng_ptr;  // blocks + 1
-  const int32_t *__restrict__ rng_lo;   // first B row of a range
-  const int32_t *__restrict__ rng_len;  // rows of a range
-  const int32_t *__restrict__ blk_rows; // staged rows of a block (-1: gathers from global)
+  const int4 *__restrict__ desc;        // blocks: {first range, ranges, p0, p1}
+  const int32_t *__restrict__ staged;   // blocks: staged band rows (-1: over budget)
+  const int4 *__restrict__ rng;         // ranges: {first B row, rows, band slot, 0}
+  const int2 *__restrict__ pairs;       // nnz (+2 pad): (slot or column, value bits)
+  const int32_t *__restrict__ rowptr;   // padded copy (n + 1 + 64)
   const float *__restrict__ B;
   float *__restrict__ C;
   int64_t ldb, ldc;
-  int32_t n_rows, K, accumulate;
+  int32_t n_rows, K, R, accumulate;
+  int64_t nblk;
   Fanout fan;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ void bulk(uint32_t dst, const void *src, uint32_t bytes,
+                                     uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -67,14 +80,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ int lda(const int32_t *p) {
-  int v;
-  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ float lda(const float *p) {
-  float v;
-  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
   return v;
 }
 __device__ __forceinline__ void fma4(float4 &acc, float v, const float4 &b) {
@@ -84,104 +94,121 @@ __device__ __forceinline__ void fma4(float4 &acc, float v, const float4 &b) {
   acc.w = fmaf(v, b.w, acc.w);
 }
 
-// G lanes per row (K <= 4 G), RPG rows per group: kRows = kWarps (32 / G) RPG.
+// G lanes per row (K <= 4 G).  Persistent CTAs: warp 4 is the producer —
+// per block (b = blockIdx.x, + gridDim.x, ...) it reads the descriptor,
+// writes the block's info into the stage, arms the stage's mbarrier with the
+// byte count and issues every copy (one range per lane); warps 0-3 (128
+// threads = 128 / G row groups) compute the block of the other stage.  Two
+// stages, so the next block's copies are in flight while this one computes.
+constexpr int kStages = 2;
+constexpr int kStageBytes = kBandBytes + kPairCap * 8 + 64 * 4 + 32;  // + info
+constexpr int kSmem = kStages * kStageBytes + 64;                      // + barriers
+
 template <int G>
-__global__ void __launch_bounds__(kThreads, 3) spmm_band_kernel(const BandArgs a) {
-  constexpr int GPW = 32 / G;                  // row groups per warp
-  constexpr int RPG = kRows / (kWarps * GPW);  // rows per group
+__global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane / G, l = lane % G;
-  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
-  const int blk = blockIdx.x;
-  const int64_t r0 = (int64_t)blk * kRows;
-  const int staged = a.blk_rows[blk];
+  constexpr int GROUPS = kThreads / G;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rowb = (uint32_t)a.ldb * 4u;  // staged row pitch = B's row pitch
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+  const int64_t nblk = a.nblk;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[s])),
+                   "r"(kThreads));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0 && staged > 0) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
-                 "r"((uint32_t)staged * rowb)
-                 : "memory");
-    uint32_t dst = smem_u32(smem);
-    for (int i = a.rng_ptr[blk], e = a.rng_ptr[blk + 1]; i < e; ++i) {
-      const uint32_t bytes = (uint32_t)a.rng_len[i] * rowb;
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-          "[%3];" ::"r"(dst),
-          "l"(a.B + (int64_t)a.rng_lo[i] * a.ldb), "r"(bytes), "r"(smem_u32(&bar))
-          : "memory");
-      dst += bytes;
+
+  if (warp == kThreads / 32) {  // producer warp
+    int it = 0;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+      const int s = it & 1;
+      unsigned char *st = smem + s * kStageBytes;
+      int *info = reinterpret_cast<int *>(st + kBandBytes + kPairCap * 8 + 64 * 4);
+      if (it >= kStages) mbar_wait_parity(&empty[s], ((it >> 1) - 1) & 1);
+      const int4 d = a.desc[blk];
+      const int staged = a.staged[blk];
+      const int64_t r0 = blk * a.R;
+      const int rows = (int)(a.n_rows - r0 < a.R ? a.n_rows - r0 : a.R);
+      const int pb = d.z & ~1, pcnt = (d.w - pb + 1) & ~1;  // 16-B aligned pair run
+      const bool pairs_in = pcnt <= kPairCap;
+      const int rp_cnt = (rows + 3) & ~3;
+      if (lane == 0) {
+        info[0] = staged;
+        info[1] = pairs_in ? pb : -1;
+        info[2] = d.w;
+        info[3] = rows;
+        const uint32_t bytes = (staged > 0 ? (uint32_t)staged * rowb : 0u) +
+                               (pairs_in ? (uint32_t)pcnt * 8u : 0u) + (uint32_t)rp_cnt * 4u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         smem_u32(&full[s])),
+                     "r"(bytes)
+                     : "memory");
+      }
+      __syncwarp();
+      const uint32_t bar = smem_u32(&full[s]);
+      if (staged > 0)
+        for (int i = lane; i < d.y; i += 32) {
+          const int4 r = a.rng[d.x + i];
+          bulk(smem_u32(st) + (uint32_t)r.z * rowb, a.B + (int64_t)r.x * a.ldb,
+               (uint32_t)r.y * rowb, bar);
+        }
+      if (lane == 0 && pairs_in && pcnt > 0)
+        bulk(smem_u32(st + kBandBytes), a.pairs + pb, (uint32_t)pcnt * 8u, bar);
+      if (lane == 1)
+        bulk(smem_u32(st + kBandBytes + kPairCap * 8), a.rowptr + r0, (uint32_t)rp_cnt * 4u, bar);
     }
+    return;
   }
-  // A of this group's rows into registers while the band lands
-  int p0[RPG], cnt[RPG], sl[RPG];
-  float vv[RPG];
-#pragma unroll
-  for (int i = 0; i < RPG; ++i) {
-    const int64_t r = r0 + (i * kWarps + warp) * GPW + g;
-    const bool ok = r < a.n_rows;
-    p0[i] = ok ? lda(a.rowptr + r) : 0;
-    cnt[i] = ok ? lda(a.rowptr + r + 1) - p0[i] : 0;
-  }
-#pragma unroll
-  for (int i = 0; i < RPG; ++i) {
-    const bool ok = l < cnt[i];
-    sl[i] = ok ? lda(a.slot + p0[i] + l) : 0;
-    vv[i] = ok ? lda(a.val + p0[i] + l) : 0.f;
-  }
+
+  const int g = tid / G, l = tid % G;
   const bool cok = l * 4 < a.K;
-  const uint32_t sbase = smem_u32(smem) + l * 16;
   const float *gb = a.B + l * 4;
-  if (staged > 0) mbar_wait(&bar, 0);
-#pragma unroll
-  for (int i = 0; i < RPG; ++i) {
-    const int64_t r = r0 + (i * kWarps + warp) * GPW + g;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int n = cnt[i];
-    const int nb = min(n, G);
-    if (staged > 0) {
-      for (int j = 0; j < nb; ++j) {
-        const int s = __shfl_sync(gmask, sl[i], j, G);
-        const float v = __shfl_sync(gmask, vv[i], j, G);
-        if (cok) {
-          float4 b;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
-                       : "r"(sbase + (uint32_t)s * rowb));
-          fma4(acc, v, b);
+  int it = 0;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+    const int s = it & 1;
+    unsigned char *st = smem + s * kStageBytes;
+    const int2 *spairs = reinterpret_cast<const int2 *>(st + kBandBytes);
+    const int32_t *srp = reinterpret_cast<const int32_t *>(st + kBandBytes + kPairCap * 8);
+    const int *info = reinterpret_cast<const int *>(st + kBandBytes + kPairCap * 8 + 64 * 4);
+    mbar_wait_parity(&full[s], (it >> 1) & 1);
+    const int staged = info[0], pb = info[1], p_end = info[2], rows = info[3];
+    const int64_t r0 = blk * a.R;
+    const uint32_t sb = smem_u32(st) + l * 16;
+    for (int i = g; i < rows; i += GROUPS) {
+      if (!cok) break;
+      const int q0 = srp[i], q1 = i + 1 < rows ? srp[i + 1] : p_end;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (pb >= 0 && staged > 0) {  // pairs and band in shared memory (the fast path)
+        const int2 *pp = spairs + (q0 - pb);
+        const int n = q1 - q0;
+        int j = 0;
+        for (; j + 2 <= n; j += 2) {
+          const int2 x = pp[j], y = pp[j + 1];
+          const float4 bx = lds4(sb + (uint32_t)x.x * rowb), by = lds4(sb + (uint32_t)y.x * rowb);
+          fma4(acc, __int_as_float(x.y), bx);
+          fma4(acc, __int_as_float(y.y), by);
+        }
+        if (j < n) {
+          const int2 x = pp[j];
+          fma4(acc, __int_as_float(x.y), lds4(sb + (uint32_t)x.x * rowb));
+        }
+      } else {  // a pair run over the stage or a band over budget: the global forms
+        for (int j = q0; j < q1; ++j) {
+          const int2 x = pb >= 0 ? spairs[j - pb] : __ldg(a.pairs + j);
+          const float4 b = staged > 0
+                               ? lds4(sb + (uint32_t)x.x * rowb)
+                               : __ldg(reinterpret_cast<const float4 *>(gb + (int64_t)x.x * a.ldb));
+          fma4(acc, __int_as_float(x.y), b);
         }
       }
-      for (int j = G; j < n && cok; ++j) {  // rows longer than G vectors
-        const int s = lda(a.slot + p0[i] + j);
-        const float v = lda(a.val + p0[i] + j);
-        float4 b;
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
-                     : "r"(sbase + (uint32_t)s * rowb));
-        fma4(acc, v, b);
-      }
-    } else {  // band over budget: gather from global (slot = column)
-      for (int j = 0; j < nb; ++j) {
-        const int s = __shfl_sync(gmask, sl[i], j, G);
-        const float v = __shfl_sync(gmask, vv[i], j, G);
-        if (cok) fma4(acc, v, __ldg(reinterpret_cast<const float4 *>(gb + (int64_t)s * a.ldb)));
-      }
-      for (int j = G; j < n && cok; ++j) {
-        const int s = lda(a.slot + p0[i] + j);
-        const float v = lda(a.val + p0[i] + j);
-        fma4(acc, v, __ldg(reinterpret_cast<const float4 *>(gb + (int64_t)s * a.ldb)));
-      }
-    }
-    if (r < a.n_rows && cok) {
-      const int64_t off = r * a.ldc + l * 4;
-      float4 *p = reinterpret_cast<float4 *>(a.C + off);
+      const int64_t off = (r0 + i) * a.ldc + l * 4;
       if (a.accumulate) {
-        const float4 o = *p;
+        const float4 o = *reinterpret_cast<const float4 *>(a.C + off);
         acc.x += o.x;
         acc.y += o.y;
         acc.z += o.z;
@@ -189,6 +216,10 @@ __global__ void __launch_bounds__(kThreads, 3) spmm_band_kernel(const BandArgs a
       }
       fan_store4(a.C, a.fan, off, acc);
     }
+    // the stage is refilled by bulk copies (async proxy): order this thread's
+    // generic reads before its release (WAR across proxies)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
   }
   if (a.fan.n) __threadfence_system();
 }
@@ -208,10 +239,14 @@ int lanes_for(int K) {
 }
 
 template <int G>
-pspmm_status launch_band(const BandArgs &args, int64_t nblk, size_t smem, cudaStream_t stream) {
+pspmm_status launch_band(const BandArgs &args, int64_t nblk, cudaStream_t stream) {
   PSPMM_CUDA_TRY(cudaFuncSetAttribute(spmm_band_kernel<G>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  spmm_band_kernel<G><<<(unsigned)nblk, kThreads, smem, stream>>>(args);
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+  int per_sm = 0;
+  PSPMM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_band_kernel<G>,
+                                                               kThreads + 32, kSmem));
+  const int64_t grid = std::min<int64_t>(nblk, (int64_t)num_sms() * std::max(1, per_sm));
+  spmm_band_kernel<G><<<(unsigned)grid, kThreads + 32, kSmem, stream>>>(args);
   PSPMM_CUDA_TRY(cudaGetLastError());
   return PSPMM_OK;
 }
@@ -220,17 +255,15 @@ pspmm_status launch_band(const BandArgs &args, int64_t nblk, size_t smem, cudaSt
 
 void destroy_band(Band *D) {
   if (!D) return;
-  cudaFree(D->d_slot);
-  cudaFree(D->d_rng_ptr);
-  cudaFree(D->d_rng_lo);
-  cudaFree(D->d_rng_len);
-  cudaFree(D->d_blk_rows);
+  cudaFree(D->d_desc);
+  cudaFree(D->d_staged);
+  cudaFree(D->d_rng);
+  cudaFree(D->d_pairs);
+  cudaFree(D->d_rowptr);
   delete D;
 }
 
-// Host pack: per block of kRows rows the merged column ranges and the
-// nonzeros' band slots (blocks split over host threads).  Synchronises
-// `stream`.
+// Host pack (blocks split over host threads).  Synchronises `stream`.
 pspmm_status attach_band(pspmm_pcsr_s *A, int32_t k_max, cudaStream_t stream, double *staged_frac) {
   if (!A) PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "attach_band: null handle");
   if (A->V != 1 || A->S != 0)
@@ -238,64 +271,73 @@ pspmm_status attach_band(pspmm_pcsr_s *A, int32_t k_max, cudaStream_t stream, do
   if (k_max < 4 || k_max > kBandMaxK || k_max % 4 != 0)
     PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "attach_band: k_max must be a multiple of 4 in [4, 128]");
   const int64_t n = A->n_rows, nnz = A->nnz;
-  const int64_t nblk = (n + kRows - 1) / kRows;
+  if (nnz >= 0x7ffffff0ll) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "attach_band: nnz >= 2^31");
+  const int R = block_rows(k_max);
+  const int64_t nblk = (n + R - 1) / R;
   const int64_t max_rows = kBandBytes / ((int64_t)k_max * 4);  // staged rows per block
   PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
-  std::vector<int32_t> rp(n + 1), ci(nnz);
+  std::vector<int32_t> rp(n + 1 + 64), ci(nnz);
+  std::vector<float> vl(nnz);
   PSPMM_CUDA_TRY(cudaMemcpy(rp.data(), A->d_rowptr, (n + 1) * 4, cudaMemcpyDeviceToHost));
-  if (nnz) PSPMM_CUDA_TRY(cudaMemcpy(ci.data(), A->d_colidx, nnz * 4, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> slot(std::max<int64_t>(nnz, 1)), blk_rows(nblk);
-  std::vector<std::vector<int32_t>> lo_t(nblk), len_t(nblk);
+  for (int k = 0; k < 64; ++k) rp[n + 1 + k] = rp[n];
+  if (nnz) {
+    PSPMM_CUDA_TRY(cudaMemcpy(ci.data(), A->d_colidx, nnz * 4, cudaMemcpyDeviceToHost));
+    PSPMM_CUDA_TRY(cudaMemcpy(vl.data(), A->d_val, nnz * 4, cudaMemcpyDeviceToHost));
+  }
+  std::vector<int2> pairs(nnz + 2, make_int2(0, 0));
+  std::vector<int4> desc(nblk);
+  std::vector<int32_t> staged(nblk);
+  std::vector<std::vector<int4>> rng_t(nblk);
   const int nth = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   std::vector<std::thread> th;
   for (int t = 0; t < nth; ++t)
     th.emplace_back([&, t] {
       std::vector<int32_t> cols;
       for (int64_t b = t; b < nblk; b += nth) {
-        const int64_t q0 = rp[b * kRows], q1 = rp[std::min(n, (b + 1) * kRows)];
+        const int64_t q0 = rp[b * R], q1 = rp[std::min(n, (b + 1) * R)];
         cols.assign(ci.begin() + q0, ci.begin() + q1);
         std::sort(cols.begin(), cols.end());
         cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
-        std::vector<int32_t> &lo = lo_t[b], &len = len_t[b];
+        std::vector<int4> &rg = rng_t[b];
         int64_t rows = 0;
         for (size_t i = 0; i < cols.size();) {
           size_t j = i;
           while (j + 1 < cols.size() && cols[j + 1] - cols[j] <= kGap + 1) ++j;
-          lo.push_back(cols[i]);
-          len.push_back(cols[j] - cols[i] + 1);
+          rg.push_back(make_int4(cols[i], cols[j] - cols[i] + 1, (int)rows, 0));
           rows += cols[j] - cols[i] + 1;
           i = j + 1;
         }
-        if (rows > max_rows || rows == 0) {  // over budget (or empty): global gathers
-          blk_rows[b] = rows == 0 ? 0 : -1;
-          lo.clear();
-          len.clear();
-          for (int64_t p = q0; p < q1; ++p) slot[p] = ci[p];
-          continue;
-        }
-        blk_rows[b] = (int32_t)rows;
-        // column -> slot: ranges are sorted; slot = range base + offset
-        std::vector<int64_t> base(lo.size());
-        int64_t acc = 0;
-        for (size_t k = 0; k < lo.size(); ++k) {
-          base[k] = acc;
-          acc += len[k];
-        }
+        const bool fits = rows > 0 && rows <= max_rows;
+        staged[b] = rows == 0 ? 0 : fits ? (int32_t)rows : -1;
+        if (!fits) rg.clear();
         for (int64_t p = q0; p < q1; ++p) {
-          const size_t k = std::upper_bound(lo.begin(), lo.end(), ci[p]) - lo.begin() - 1;
-          slot[p] = (int32_t)(base[k] + (ci[p] - lo[k]));
+          int32_t s = ci[p];
+          if (fits) {  // column -> band slot (ranges sorted by first row)
+            size_t lo = 0, hi = rg.size();
+            while (hi - lo > 1) {
+              const size_t mid = (lo + hi) / 2;
+              if (rg[mid].x <= s)
+                lo = mid;
+              else
+                hi = mid;
+            }
+            s = rg[lo].z + (s - rg[lo].x);
+          }
+          int32_t bits;
+          std::memcpy(&bits, &vl[p], 4);
+          pairs[p] = make_int2(s, bits);
         }
       }
     });
   for (auto &x : th) x.join();
-  std::vector<int32_t> rng_ptr(nblk + 1, 0), rng_lo, rng_len;
+  std::vector<int4> rng;
   int64_t staged_blocks = 0, nonempty = 0;
   for (int64_t b = 0; b < nblk; ++b) {
-    rng_ptr[b + 1] = rng_ptr[b] + (int32_t)lo_t[b].size();
-    rng_lo.insert(rng_lo.end(), lo_t[b].begin(), lo_t[b].end());
-    rng_len.insert(rng_len.end(), len_t[b].begin(), len_t[b].end());
-    if (blk_rows[b] != 0) ++nonempty;
-    if (blk_rows[b] > 0) ++staged_blocks;
+    const int64_t q0 = rp[b * R], q1 = rp[std::min(n, (b + 1) * R)];
+    desc[b] = make_int4((int)rng.size(), (int)rng_t[b].size(), (int)q0, (int)q1);
+    rng.insert(rng.end(), rng_t[b].begin(), rng_t[b].end());
+    if (staged[b] != 0) ++nonempty;
+    if (staged[b] > 0) ++staged_blocks;
   }
   Band *D = new Band();
   struct Guard {
@@ -304,13 +346,14 @@ pspmm_status attach_band(pspmm_pcsr_s *A, int32_t k_max, cudaStream_t stream, do
   } guard{D};
   D->num_blocks = nblk;
   D->k_max = k_max;
+  D->rows = R;
   D->staged_frac = nonempty ? (double)staged_blocks / nonempty : 1.0;
   pspmm_status st;
-  if ((st = upload(&D->d_slot, slot)) != PSPMM_OK) return st;
-  if ((st = upload(&D->d_rng_ptr, rng_ptr)) != PSPMM_OK) return st;
-  if ((st = upload(&D->d_rng_lo, rng_lo)) != PSPMM_OK) return st;
-  if ((st = upload(&D->d_rng_len, rng_len)) != PSPMM_OK) return st;
-  if ((st = upload(&D->d_blk_rows, blk_rows)) != PSPMM_OK) return st;
+  if ((st = upload(&D->d_desc, desc)) != PSPMM_OK) return st;
+  if ((st = upload(&D->d_staged, staged)) != PSPMM_OK) return st;
+  if ((st = upload(&D->d_rng, rng)) != PSPMM_OK) return st;
+  if ((st = upload(&D->d_pairs, pairs)) != PSPMM_OK) return st;
+  if ((st = upload(&D->d_rowptr, rp)) != PSPMM_OK) return st;
   destroy_band(A->band);
   A->band = D;
   guard.d = nullptr;
@@ -336,28 +379,26 @@ pspmm_status run_spmm_band(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb,
   const Band *D = A->band;
   if (D->num_blocks == 0) return PSPMM_OK;
   BandArgs args;
-  args.rowptr = A->d_rowptr;
-  args.slot = D->d_slot;
-  args.val = A->d_val;
-  args.rng_ptr = D->d_rng_ptr;
-  args.rng_lo = D->d_rng_lo;
-  args.rng_len = D->d_rng_len;
-  args.blk_rows = D->d_blk_rows;
+  args.desc = D->d_desc;
+  args.staged = D->d_staged;
+  args.rng = D->d_rng;
+  args.pairs = D->d_pairs;
+  args.rowptr = D->d_rowptr;
   args.B = d_B;
   args.C = d_C;
   args.ldb = ldb;
   args.ldc = ldc;
   args.n_rows = (int32_t)A->n_rows;
   args.K = K;
+  args.R = D->rows;
   args.accumulate = accumulate;
+  args.nblk = D->num_blocks;
   args.fan = fan;
-  // dynamic shared memory: the largest band this k_max allows at this pitch
-  const size_t smem = (size_t)(kBandBytes / ((int64_t)D->k_max * 4)) * (size_t)ldb * 4;
   switch (lanes_for(K)) {
-    case 4: return launch_band<4>(args, D->num_blocks, smem, stream);
-    case 8: return launch_band<8>(args, D->num_blocks, smem, stream);
-    case 16: return launch_band<16>(args, D->num_blocks, smem, stream);
-    default: return launch_band<32>(args, D->num_blocks, smem, stream);
+    case 4: return launch_band<4>(args, D->num_blocks, stream);
+    case 8: return launch_band<8>(args, D->num_blocks, stream);
+    case 16: return launch_band<16>(args, D->num_blocks, stream);
+    default: return launch_band<32>(args, D->num_blocks, stream);
   }
 }
 

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NW);
+      mbar_init(&empty[s], NW * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -256,8 +256,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     mbar_wait(&full[s], (t / kStages) & 1);
 #pragma unroll
     for (int r = 0; r < RW; ++r) row_window(acc[r], pa, cnt.get(r), tile);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    // the stage is refilled by TMA / bulk copies (async proxy) after the
+    // release: every lane orders its own generic reads before it (WAR across
+    // proxies) and arrives itself, so the release covers each lane's reads
+    // without relying on __syncwarp cumulativity
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(&empty[s]);
     cnt = nxt;
     woff = woff_n;
   }

@@ -39,7 +39,7 @@ def parse_header():
 def walk(model, f, K):
     """Majority vote of the forest, ties to the lowest label id."""
     _, roots, feat, thr, left, right, leaf, labs = model
-    x = [f[k] for k in FEATS] + [math.log2(K)]
+    x = [f[k] for k in FEATS] + [math.log2(K), math.log2(max(f["n"], 1.0) * K * 4.0 / L2_B200)]
     votes = [0] * len(labs)
     for node in roots:
         while feat[node] >= 0:

@@ -42,13 +42,13 @@ GRAPHS = {
 }
 
 
-def _run(g, K, k_max=128, pad=0, accumulate=False, n_cols=None, seed=3):
+def _run(g, K, k_max=None, pad=0, accumulate=False, n_cols=None, seed=3):
     import torch
     from paper_2605_15695_b200 import api
     rp, ci, vl = dev(g)
     nc = n_cols or g.n
     A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, 1, 0, n_cols=nc)
-    frac = api.pspmm_pcsr_attach_band(A, k_max)
+    frac = api.pspmm_pcsr_attach_band(A, k_max or max(4, K + pad))
     B = gen.dense(nc, K, seed)
     Bb = torch.zeros((nc, K + pad), device="cuda")
     Bb[:, :K] = torch.from_numpy(B).cuda()
@@ -74,8 +74,8 @@ def test_band_engine_parity(name, K):
     assert 0.0 <= frac <= 1.0
     if name in ("roadnet_small", "banded"):
         assert frac == 1.0
-    if name == "shuffled":
-        assert frac < 0.5  # the global-gather path is exercised
+    if name == "shuffled" and K >= 8:
+        assert frac < 0.5  # the global-gather path is exercised (4000 rows x K x 4 B > 64 KB)
 
 
 @pytest.mark.parametrize("name", ["roadnet_small", "shuffled", "hubs"])
@@ -102,8 +102,7 @@ def test_band_engine_all_positive_long_rows():
     """c-24 stress: all-positive values, rows of ~2000 nonzeros in one band."""
     g = _graph_rect(400, 2400, 0.85, 14, band=1200)
     g.val = gen.values(g.nnz, 15, "positive")
-    _, _, B, C, _ = _run(g, 64, seed=16)
-    B2 = np.abs(B)
+    B2 = np.abs(gen.dense(2400, 64, 16))
     import torch
     from paper_2605_15695_b200 import api
     rp, ci, vl = dev(g)

@@ -1,6 +1,7 @@
 """speedup over cuSPARSE (best CSR algorithm) across the K
-sweep, per workload, with the decided config at each K (forest + mode-1
-rule), L2 flushed between launches.  One JSON line per (workload, K), then a
+sweep, per workload, with the config the library selects at each K (forest
++ guards, then the mode-1 / mode-5 / mode-6 rules, as bench.py), L2 flushed
+between launches.  One JSON line per (workload, K), then a
 summary line with the geomeans.
 
 python tools/k_sweep.py --workloads cora,roadnet,products,proteins,reddit --Ks 16,32,64,128,256
@@ -44,6 +45,8 @@ def main():
             A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, cfg.V, cfg.S, cfg.omega,
                                      cfg.sg_override)
             cfg, dense = api.auto_dense(A, rp, ci, vl, K, cfg)
+            cfg, A, _ = api.auto_blocks(A, rp, ci, vl, K, cfg)   # mode 5 rule
+            cfg, A, _ = api.auto_band(A, rp, ci, vl, K, cfg, feats)  # mode 6 rule
             B = torch.from_numpy(gen.dense(g.n, K, 7000 + K)).cuda()
             C = torch.empty((g.n, K), device="cuda")
             ts = bench.time_steps(lambda: A.run(B, C, cfg), a.steps, 3, flush, stream)

@@ -79,7 +79,7 @@ def corpus_graphs(count, seed=12345, n_lo=20000, n_hi=400000, prefix=""):
 
 
 def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2, 1)), modes=(0,),
-                orders=(0,)):
+                orders=(0,), cands=None):
     import torch
     from paper_2605_15695_b200 import api
     rp = torch.from_numpy(g.rowptr).cuda()
@@ -107,6 +107,9 @@ def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2,
                         while G < -(-(K // 4) // F) and G < 32:
                             G <<= 1
                         points += [(m, W, F, max(G, 2), 0) for W in (2, 4, 8)]
+            if cands is not None:  # restricted sweep: the per-K candidate labels only
+                points = [(m, W, F, G, o) for (v, s_, W, F, G, m, o) in cands.get(K, ())
+                          if (v, s_) == (V, S)]
             for (mode, W, F, G, order) in points:
                 cfg = api.Config(W=W, F=max(F, 1), V=V, S=S, G=G, mode=mode, order=order)
                 evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -215,6 +218,9 @@ def main():
                     help="sweep files whose top labels to re-time (graphs: --workloads names "
                          "and --corpus N regenerated)")
     ap.add_argument("--top", type=int, default=8)
+    ap.add_argument("--candidates", nargs="*", default=None,
+                    help="sweep files: restrict the lattice to the labels within 2 %% of the "
+                         "best of some record at the same K (large graphs)")
     a = ap.parse_args()
     Ws = tuple(int(x) for x in a.Ws.split(","))
     VS = tuple((int(x[0]), int(x[1])) for x in a.VS.split(","))
@@ -256,11 +262,24 @@ def main():
         print(f"[{time.time() - t0:.0f}s] {name}: best {recs[-1]['best']} "
               f"{recs[-1]['best_gflops']:.0f} GFLOP/s", flush=True)
         json.dump(recs, open(a.out, "w"))
+    cands = None
+    if a.candidates:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from train_decider import load
+        cands = {}
+        for r in load(a.candidates):
+            b = min(t["ms"] for t in r["table"])
+            for t in r["table"]:
+                if t["ms"] <= 1.02 * b:
+                    cands.setdefault(r["K"], set()).add(
+                        (t["V"], t["S"], t["W"], t["F"], t["G"], t.get("mode", 0),
+                         t.get("order", 0)))
+        print({K: len(v) for K, v in cands.items()}, flush=True)
     if a.corpus:
         Ks = [int(k) for k in a.Ks.split(",")] if a.Ks else [16, 32, 64, 128, 256]
         lo, hi = (int(x) for x in a.corpus_n.split(","))
         for g in corpus_graphs(a.corpus, a.corpus_seed, lo, hi, a.corpus_prefix):
-            recs += sweep_graph(g, Ks, a.iters, flush, stream, Ws, VS, modes, orders)
+            recs += sweep_graph(g, Ks, a.iters, flush, stream, Ws, VS, modes, orders, cands)
             print(f"[{time.time() - t0:.0f}s] {g.name} n={g.n} nnz={g.nnz}", flush=True)
             json.dump(recs, open(a.out, "w"))
     json.dump(recs, open(a.out, "w"))
