@@ -138,6 +138,8 @@ struct GemmArgs {
   float *__restrict__ T;
   int64_t n, ldx, ldw, ldt;
   int32_t Ki, Ko, raw_stages, tmem_cols;
+  int32_t stage_out;  // 1: the epilogue stages the tile in shared memory (coalesced rows)
+  int32_t op_stages;  // split-operand ring depth (2..4)
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -145,12 +147,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-  const int Ki = a.Ki, Ko = a.Ko, S = kOpStages, R = a.raw_stages;
+  const int Ki = a.Ki, Ko = a.Ko, S = a.op_stages, R = a.raw_stages;
   const uint32_t wpart = (uint32_t)Ki * Ko * 4;  // one part of W's image
   uint8_t *raw0 = smem;                          // R x 16 KB raw X chunks (1 KB aligned)
   uint8_t *stage0 = raw0 + (size_t)R * kRawBytes;  // S x [hi 16 KB | lo 16 KB]
   uint8_t *wimg = stage0 + (size_t)S * kChunkBytes;  // [hi | lo], each [Ki/4][Ko][4]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(wimg + 2 * wpart);
+  uint8_t *otile = wimg + 2 * wpart;  // stage_out: 128 rows x Ko fp32, 16-B chunks swizzled
+  uint64_t *bar = reinterpret_cast<uint64_t *>(otile + (a.stage_out ? (size_t)kM * Ko * 4 : 0));
   uint64_t *full = bar, *empty = bar + S, *accf = bar + 2 * S, *acce = bar + 2 * S + 2;
   uint64_t *rfull = bar + 2 * S + 4, *rempty = rfull + R;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + R);
@@ -282,8 +285,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = tl & 1;
       mbar_wait(&accf[b], (tl >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int64_t row = t * kM + quarter * 32 + lane;
+      const int rloc = quarter * 32 + lane;
+      const int64_t row = t * kM + rloc;
       const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * Ko);
+      if (a.stage_out) {
+        // TMEM -> shared tile (thread = row; 16-B chunk j of row r stored at
+        // chunk j ^ (r % 8) of its 128-B group: 4 wavefronts per warp store)
+        const int q = Ko / 4;  // 16-B chunks per row
+        for (int c = 0; c < Ko; c += 16) {
+          float v[16];
+          tmem_ld16(tb + c, v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int ch = c / 4 + j, sw = (ch & ~7) | ((ch ^ rloc) & 7);
+            *reinterpret_cast<float4 *>(otile + ((size_t)rloc * q + sw) * 16) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&acce[b]);  // TMEM buffer free: the next tile's MMAs may start
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+        // shared tile -> T, row-contiguous: a warp stores 512 consecutive bytes
+        const int e = tid - (kLoaders + 32);  // 0..127
+        for (int idx = e; idx < kM * q; idx += kEpi) {
+          const int r = idx / q, ch = idx % q, sw = (ch & ~7) | ((ch ^ r) & 7);
+          const int64_t grow = t * kM + r;
+          if (grow < a.n)
+            __stcs(reinterpret_cast<float4 *>(a.T + grow * a.ldt) + ch,
+                   *reinterpret_cast<const float4 *>(otile + ((size_t)r * q + sw) * 16));
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+        continue;
+      }
       for (int c = 0; c < Ko; c += 16) {
         float v[16];
         tmem_ld16(tb + c, v);
@@ -333,12 +366,21 @@ pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_
   if (n == 0) return PSPMM_OK;
   if (n > 0x7fffffffll) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "dense_gemm: n >= 2^31");
   const int64_t w = 2ll * Ki * Ko * 4;
-  int raw = (int)std::min<int64_t>(
-      8, (kMaxSmem - 1024 - 512 - w - (int64_t)kOpStages * kChunkBytes) / kRawBytes);
+  // the staged epilogue (coalesced row stores) when its tile fits beside two
+  // raw stages (Ko % 32 == 0, so 16-B chunks swizzle within 128-B groups)
+  int ops = kOpStages;
+  if (const char *e = std::getenv("PSPMM_GEMM_OPS"))  // A/B knob for the tools (2..4)
+    ops = std::max(2, std::min(4, std::atoi(e)));
+  while (ops > 2 && 1024 + 512 + w + (int64_t)ops * kChunkBytes + 2ll * kRawBytes > kMaxSmem) --ops;
+  const int64_t base = 1024 + 512 + w + (int64_t)ops * kChunkBytes;
+  const int64_t otile = (int64_t)kM * Ko * 4;
+  const char *se = std::getenv("PSPMM_GEMM_STAGE_OUT");  // A/B knob for the tools (0 = off)
+  const bool stage_out = !(se && se[0] == '0') && Ko % 32 == 0 &&
+                         base + otile + 2ll * kRawBytes <= kMaxSmem;
+  int raw = (int)std::min<int64_t>(8, (kMaxSmem - base - (stage_out ? otile : 0)) / kRawBytes);
   if (const char *e = std::getenv("PSPMM_GEMM_RAW"))  // A/B knob for the tools (2..raw)
     raw = std::max(2, std::min(raw, std::atoi(e)));
-  const size_t smem =
-      (size_t)(w + (int64_t)kOpStages * kChunkBytes + (int64_t)raw * kRawBytes + 1024 + 512);
+  const size_t smem = (size_t)(base + (stage_out ? otile : 0) + (int64_t)raw * kRawBytes);
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
   if (!encode) PSPMM_FAIL(PSPMM_ERR_CUDA, "dense_gemm: cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
@@ -363,6 +405,8 @@ pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_
   args.Ki = Ki;
   args.Ko = Ko;
   args.raw_stages = raw;
+  args.stage_out = stage_out ? 1 : 0;
+  args.op_stages = ops;
   args.tmem_cols = tmem_cols_for(Ko);
   const int64_t tiles = (n + kM - 1) / kM;
   const int grid = (int)std::min<int64_t>(tiles, num_sms());

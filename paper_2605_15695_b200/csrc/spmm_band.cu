@@ -32,6 +32,7 @@
 //
 // The pack is derived data, not part of the bit-exact PCSR contract.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -58,6 +59,7 @@ struct BandArgs {
   int64_t ldb, ldc;
   int32_t n_rows, K, R, accumulate;
   int64_t nblk;
+  int32_t stages;  // stage ring depth (2 by default: 3 CTAs per SM)
   Fanout fan;
 };
 
@@ -100,21 +102,22 @@ __device__ __forceinline__ void fma4(float4 &acc, float v, const float4 &b) {
 // byte count and issues every copy (one range per lane); warps 0-3 (128
 // threads = 128 / G row groups) compute the block of the other stage.  Two
 // stages, so the next block's copies are in flight while this one computes.
-constexpr int kStages = 2;
+constexpr int kMaxStages = 4;
+constexpr int kRPG = 4;  // rows per row group in one block (R = kRPG x 128 / G at K = 4 G)
 constexpr int kStageBytes = kBandBytes + kPairCap * 8 + 64 * 4 + 32;  // + info
-constexpr int kSmem = kStages * kStageBytes + 64;                      // + barriers
 
 template <int G>
 __global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int GROUPS = kThreads / G;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
-  uint64_t *empty = full + kStages;
+  const int S = a.stages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * kStageBytes);
+  uint64_t *empty = full + kMaxStages;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rowb = (uint32_t)a.ldb * 4u;  // staged row pitch = B's row pitch
   const int64_t nblk = a.nblk;
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[s])),
                    "r"(kThreads));
@@ -124,19 +127,25 @@ __global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandA
   __syncthreads();
 
   if (warp == kThreads / 32) {  // producer warp
-    int it = 0;
-    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
-      const int s = it & 1;
+    // the next block's descriptor, staged-row count and range entries are
+    // loaded before waiting for its stage, so only the copy issue waits
+    int64_t blk = blockIdx.x;
+    int4 d = blk < nblk ? a.desc[blk] : make_int4(0, 0, 0, 0);
+    int staged = blk < nblk ? a.staged[blk] : 0;
+    int4 r = (blk < nblk && staged > 0 && lane < d.y) ? a.rng[d.x + lane] : make_int4(0, 0, 0, 0);
+    for (int it = 0; blk < nblk; ++it) {
+      const int s = it % S;
+      const int64_t nb = blk + gridDim.x;  // prefetch the next block's metadata
+      const int4 dn = nb < nblk ? a.desc[nb] : make_int4(0, 0, 0, 0);
+      const int stn = nb < nblk ? a.staged[nb] : 0;
       unsigned char *st = smem + s * kStageBytes;
       int *info = reinterpret_cast<int *>(st + kBandBytes + kPairCap * 8 + 64 * 4);
-      if (it >= kStages) mbar_wait_parity(&empty[s], ((it >> 1) - 1) & 1);
-      const int4 d = a.desc[blk];
-      const int staged = a.staged[blk];
       const int64_t r0 = blk * a.R;
       const int rows = (int)(a.n_rows - r0 < a.R ? a.n_rows - r0 : a.R);
       const int pb = d.z & ~1, pcnt = (d.w - pb + 1) & ~1;  // 16-B aligned pair run
       const bool pairs_in = pcnt <= kPairCap;
       const int rp_cnt = (rows + 3) & ~3;
+      if (it >= S) mbar_wait_parity(&empty[s], ((it / S) - 1) & 1);
       if (lane == 0) {
         info[0] = staged;
         info[1] = pairs_in ? pb : -1;
@@ -151,16 +160,24 @@ __global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandA
       }
       __syncwarp();
       const uint32_t bar = smem_u32(&full[s]);
-      if (staged > 0)
-        for (int i = lane; i < d.y; i += 32) {
-          const int4 r = a.rng[d.x + i];
+      if (staged > 0) {
+        if (lane < d.y)
           bulk(smem_u32(st) + (uint32_t)r.z * rowb, a.B + (int64_t)r.x * a.ldb,
                (uint32_t)r.y * rowb, bar);
+        for (int i = lane + 32; i < d.y; i += 32) {  // blocks with > 32 ranges
+          const int4 q = a.rng[d.x + i];
+          bulk(smem_u32(st) + (uint32_t)q.z * rowb, a.B + (int64_t)q.x * a.ldb,
+               (uint32_t)q.y * rowb, bar);
         }
+      }
       if (lane == 0 && pairs_in && pcnt > 0)
         bulk(smem_u32(st + kBandBytes), a.pairs + pb, (uint32_t)pcnt * 8u, bar);
       if (lane == 1)
         bulk(smem_u32(st + kBandBytes + kPairCap * 8), a.rowptr + r0, (uint32_t)rp_cnt * 4u, bar);
+      blk = nb;
+      d = dn;
+      staged = stn;
+      r = (blk < nblk && staged > 0 && lane < d.y) ? a.rng[d.x + lane] : make_int4(0, 0, 0, 0);
     }
     return;
   }
@@ -170,41 +187,67 @@ __global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandA
   const float *gb = a.B + l * 4;
   int it = 0;
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
-    const int s = it & 1;
+    const int s = it % S;
     unsigned char *st = smem + s * kStageBytes;
     const int2 *spairs = reinterpret_cast<const int2 *>(st + kBandBytes);
     const int32_t *srp = reinterpret_cast<const int32_t *>(st + kBandBytes + kPairCap * 8);
     const int *info = reinterpret_cast<const int *>(st + kBandBytes + kPairCap * 8 + 64 * 4);
-    mbar_wait_parity(&full[s], (it >> 1) & 1);
+    mbar_wait_parity(&full[s], (it / S) & 1);
     const int staged = info[0], pb = info[1], p_end = info[2], rows = info[3];
     const int64_t r0 = blk * a.R;
     const uint32_t sb = smem_u32(st) + l * 16;
+    if (pb >= 0 && staged > 0 && rows <= GROUPS * kRPG) {
+      // the fast path: the group's (up to kRPG) rows walked together, one
+      // nonzero of each per step, so their LDS chains overlap
+      int q0[kRPG], n[kRPG];
+      float4 acc[kRPG];
+      int nmax = 0;
+#pragma unroll
+      for (int u = 0; u < kRPG; ++u) {
+        const int i = g + u * GROUPS;
+        const bool ok = i < rows;
+        q0[u] = ok ? srp[i] - pb : 0;
+        n[u] = ok ? (i + 1 < rows ? srp[i + 1] : p_end) - pb - q0[u] : 0;
+        nmax = max(nmax, n[u]);
+        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (cok) {
+        for (int j = 0; j < nmax; ++j) {
+#pragma unroll
+          for (int u = 0; u < kRPG; ++u)
+            if (j < n[u]) {
+              const int2 x = spairs[q0[u] + j];
+              fma4(acc[u], __int_as_float(x.y), lds4(sb + (uint32_t)x.x * rowb));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kRPG; ++u) {
+          const int i = g + u * GROUPS;
+          if (i < rows) {
+            const int64_t off = (r0 + i) * a.ldc + l * 4;
+            float4 v = acc[u];
+            if (a.accumulate) {
+              const float4 o = *reinterpret_cast<const float4 *>(a.C + off);
+              v.x += o.x;
+              v.y += o.y;
+              v.z += o.z;
+              v.w += o.w;
+            }
+            fan_store4(a.C, a.fan, off, v);
+          }
+        }
+      }
+    } else {
     for (int i = g; i < rows; i += GROUPS) {
       if (!cok) break;
       const int q0 = srp[i], q1 = i + 1 < rows ? srp[i + 1] : p_end;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (pb >= 0 && staged > 0) {  // pairs and band in shared memory (the fast path)
-        const int2 *pp = spairs + (q0 - pb);
-        const int n = q1 - q0;
-        int j = 0;
-        for (; j + 2 <= n; j += 2) {
-          const int2 x = pp[j], y = pp[j + 1];
-          const float4 bx = lds4(sb + (uint32_t)x.x * rowb), by = lds4(sb + (uint32_t)y.x * rowb);
-          fma4(acc, __int_as_float(x.y), bx);
-          fma4(acc, __int_as_float(y.y), by);
-        }
-        if (j < n) {
-          const int2 x = pp[j];
-          fma4(acc, __int_as_float(x.y), lds4(sb + (uint32_t)x.x * rowb));
-        }
-      } else {  // a pair run over the stage or a band over budget: the global forms
-        for (int j = q0; j < q1; ++j) {
-          const int2 x = pb >= 0 ? spairs[j - pb] : __ldg(a.pairs + j);
-          const float4 b = staged > 0
-                               ? lds4(sb + (uint32_t)x.x * rowb)
-                               : __ldg(reinterpret_cast<const float4 *>(gb + (int64_t)x.x * a.ldb));
-          fma4(acc, __int_as_float(x.y), b);
-        }
+      for (int j = q0; j < q1; ++j) {  // a pair run over the stage or a band over budget
+        const int2 x = pb >= 0 ? spairs[j - pb] : __ldg(a.pairs + j);
+        const float4 b = staged > 0
+                             ? lds4(sb + (uint32_t)x.x * rowb)
+                             : __ldg(reinterpret_cast<const float4 *>(gb + (int64_t)x.x * a.ldb));
+        fma4(acc, __int_as_float(x.y), b);
       }
       const int64_t off = (r0 + i) * a.ldc + l * 4;
       if (a.accumulate) {
@@ -215,6 +258,7 @@ __global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandA
         acc.w += o.w;
       }
       fan_store4(a.C, a.fan, off, acc);
+    }
     }
     // the stage is refilled by bulk copies (async proxy): order this thread's
     // generic reads before its release (WAR across proxies)
@@ -240,6 +284,7 @@ int lanes_for(int K) {
 
 template <int G>
 pspmm_status launch_band(const BandArgs &args, int64_t nblk, cudaStream_t stream) {
+  const int kSmem = args.stages * kStageBytes + 2 * kMaxStages * 8;
   PSPMM_CUDA_TRY(cudaFuncSetAttribute(spmm_band_kernel<G>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
   int per_sm = 0;
@@ -393,6 +438,9 @@ pspmm_status run_spmm_band(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb,
   args.R = D->rows;
   args.accumulate = accumulate;
   args.nblk = D->num_blocks;
+  args.stages = 2;
+  if (const char *e = std::getenv("PSPMM_BAND_STAGES"))  // A/B knob for the tools (2..4)
+    args.stages = std::max(2, std::min(kMaxStages, std::atoi(e)));
   args.fan = fan;
   switch (lanes_for(K)) {
     case 4: return launch_band<4>(args, D->num_blocks, stream);

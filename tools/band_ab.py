@@ -55,7 +55,15 @@ def main():
             R = 4.0 * (g.n + 1) + 8.0 * g.nnz + 8.0 * g.n * K
             rec = {"workload": name, "K": K, "staged_frac": frac, "attach_s": t_attach}
             with torch.cuda.stream(stream):
-                for tag, h, c in (("decided", A, cfg), ("mode6", H, api.Config(mode=6))):
+                F3 = 1 if K <= 16 else 2
+                G3 = max(2, min(32, K // (4 * F3)))
+                runs = [("decided", A, cfg, None), ("mode3", H, api.Config(W=2, F=F3, G=G3, mode=3),
+                                                    None)]
+                runs += [(f"mode6_s{st}" if st != "2" else "mode6", H, api.Config(mode=6), st)
+                         for st in ("2", "3", "4")]
+                for tag, h, c, st in runs:
+                    if st is not None:
+                        os.environ["PSPMM_BAND_STAGES"] = st
                     cold = bench.time_steps(lambda: h.run(B, C, c, stream), a.iters, 3, flush,
                                             stream)
                     warm = bench.time_steps(lambda: h.run(B, C, c, stream), a.iters, 3,

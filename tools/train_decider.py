@@ -253,9 +253,9 @@ def emit_header(path, keys, model, source):
     used = sorted({n.label for n in nodes if n.feat < 0})
     lid = {k: i for i, k in enumerate(used)}
     lines = ["// Random-forest model of the SpMM-decider (DESIGN.md section 6).",
-             f"// GENERATED by tools/train_decider.py from {os.path.basename(source)}; do not edit.",
+             f"// GENERATED by tools/train_decider.py from {source}; do not edit.",
              "#pragma once", "#define PSPMM_DECIDER_TRAINED 1",
-             f'#define PSPMM_DECIDER_SOURCE "{os.path.basename(source)}"',
+             f'#define PSPMM_DECIDER_SOURCE "{source}"',
              "namespace pspmm_model {", f"constexpr int kTrees = {len(roots)};",
              f"constexpr int kNodes = {len(nodes)};", f"constexpr int kNumLabels = {len(used)};",
              "// feature index: 0..15 = pspmm_features fields in header order, 16 = log2(K),",
@@ -338,7 +338,7 @@ def main():
     # graphs; the bench workloads stay out unless --train-workloads)
     fit_idx = [i for i in range(len(recs)) if a.train_workloads or not is_wl[i]]
     model = fit_forest(X[fit_idx], perf[fit_idx], a.trees, a.depth, a.min_leaf, mtry=a.mtry)
-    emit_header(a.out_header, keys, model, ",".join(a.inputs))
+    emit_header(a.out_header, keys, model, ",".join(os.path.basename(x) for x in a.inputs))
     print(json.dumps(report, indent=1))
     if a.eval_json:
         json.dump(report, open(a.eval_json, "w"), indent=1)
