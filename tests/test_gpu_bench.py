@@ -67,13 +67,16 @@ def test_bench_two_rank_rehearsal_gloo(exchange, port):
 
 def test_bench_two_rank_auto_times_both_legs():
     """--exchange auto on a dense-halo graph: the all-gather (row e, headline)
-    and the epilogue fan-out (f2 i) are both timed and reported."""
+    and the epilogue fan-out (f2 i) are both timed and reported; the NVLS
+    multicast leg is listed (unavailable under gloo / without a multicast
+    object, with its reason)."""
     out = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                 "--master-addr", "127.0.0.1", "--master-port", "29535", "bench.py",
                 "--workload", "cora", "--steps", "3", "--warmup", "3", "--headline-only",
                 "--dist-backend", "gloo"])
     legs = out["summary"]["exchange_legs"]
-    assert list(legs) == ["allgather", "fanout"]
+    assert list(legs) == ["allgather", "fanout", "multicast"]
+    assert "ms" in legs["multicast"] or "unavailable" in legs["multicast"], legs
     for k in ("allgather", "fanout"):
         assert legs[k]["ms"] > 0 and legs[k]["kernel_ms_max"] > 0, legs
         assert legs[k]["exchange_bytes_per_rank_max"] > 0
