@@ -48,7 +48,7 @@ constexpr int kChunkBytes = 2 * kChunkPart;
 constexpr int kRawBytes = kM * kKc * 4;  // one raw fp32 chunk: 16 KB
 constexpr int kLoaders = 128, kEpi = 128;
 constexpr int kThreads = kLoaders + 32 + kEpi + 32;  // 320: splitters, MMA, epilogue, TMA
-constexpr int kOpStages = 2;
+constexpr int kOpStages = 4;  // default split-operand ring depth (fewer if smem is short)
 constexpr int kMaxSmem = 227 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -103,6 +103,17 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
+}
+// 16 columns of this thread's TMEM lane, no wait (the caller waits once for
+// several loads: tcgen05.wait::ld)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -292,15 +303,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         // TMEM -> shared tile (thread = row; 16-B chunk j of row r stored at
         // chunk j ^ (r % 8) of its 128-B group: 4 wavefronts per warp store)
         const int q = Ko / 4;  // 16-B chunks per row
-        for (int c = 0; c < Ko; c += 16) {
-          float v[16];
-          tmem_ld16(tb + c, v);
+        for (int c0 = 0; c0 < Ko; c0 += 64) {  // up to 4 loads in flight, one wait
+          uint32_t v[4][16];
+          const int nc = Ko - c0 < 64 ? (Ko - c0) / 16 : 4;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int ch = c / 4 + j, sw = (ch & ~7) | ((ch ^ rloc) & 7);
-            *reinterpret_cast<float4 *>(otile + ((size_t)rloc * q + sw) * 16) =
-                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          }
+          for (int u = 0; u < 4; ++u)
+            if (u < nc) tmem_ld16_nowait(tb + c0 + 16 * u, v[u]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < nc) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int ch = (c0 + 16 * u) / 4 + j, sw = (ch & ~7) | ((ch ^ rloc) & 7);
+                *reinterpret_cast<uint4 *>(otile + ((size_t)rloc * q + sw) * 16) =
+                    make_uint4(v[u][4 * j], v[u][4 * j + 1], v[u][4 * j + 2], v[u][4 * j + 3]);
+              }
+            }
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         mbar_arrive(&acce[b]);  // TMEM buffer free: the next tile's MMAs may start
@@ -358,7 +377,7 @@ bool gemm_tc_supported(int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx, co
     return false;
   if (!tensor_map_encoder()) return false;
   const int64_t w = 2ll * Ki * Ko * 4;
-  return w + (int64_t)kOpStages * kChunkBytes + 2ll * kRawBytes + 1024 + 512 <= kMaxSmem;
+  return w + 2ll * kChunkBytes + 2ll * kRawBytes + 1024 + 512 <= kMaxSmem;  // >= 2 + 2 stages
 }
 
 pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
