@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -61,6 +62,19 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t s
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
+  return d;
+}
+// UMMA descriptor of a K-major operand in the 128-B swizzle layout TMA
+// writes (SWIZZLE_128B, layout type 2 at bits 61-63): 8-row x 128-B atoms,
+// SBO = 1024 B between 8-row groups, LBO unused for swizzled K-major; a K
+// step inside the 128-B row advances the start address (the hardware applies
+// the XOR on the address bits, the stage base is 1024-B aligned).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr) {
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;             // LBO (ignored)
+  d |= (uint64_t)(1024 >> 4) << 32;   // SBO
+  d |= (uint64_t)1 << 46;             // version (sm_100)
+  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
   return d;
 }
 // kind::tf32 instruction descriptor: D fp32, A / B TF32, both K-major, M = 128
@@ -193,20 +207,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // W -> hi / lo image: element (k, n) at [k / 4][n][k % 4]
-  if (tid < kLoaders) {
+  // W -> hi / lo image: element (k, n) at [k / 4][n][k % 4]; every thread
+  // has 8 W loads in flight before it splits and stores them
+  {
     const int q = Ko / 4;  // float4 per W row
-    for (int i = tid; i < Ki * q; i += kLoaders) {
-      const int k = i / q, n4 = i % q;
-      const float4 w = *reinterpret_cast<const float4 *>(a.W + (int64_t)k * a.ldw + 4 * n4);
-      float4 hi, lo;
-      split4(w, hi, lo);
-      const float h[4] = {hi.x, hi.y, hi.z, hi.w}, l[4] = {lo.x, lo.y, lo.z, lo.w};
+    const int total = Ki * q;
+    for (int base = tid; base < total; base += kThreads * 8) {
+      float4 w[8];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t off = ((uint32_t)(k >> 2) * Ko + 4 * n4 + e) * 16 + (k & 3) * 4;
-        *reinterpret_cast<float *>(wimg + off) = h[e];
-        *reinterpret_cast<float *>(wimg + wpart + off) = l[e];
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * kThreads;
+        w[u] = i < total ? __ldg(reinterpret_cast<const float4 *>(a.W + (int64_t)(i / q) * a.ldw +
+                                                                   4 * (i % q)))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * kThreads;
+        if (i >= total) break;
+        const int k = i / q, n4 = i % q;
+        float4 hi, lo;
+        split4(w[u], hi, lo);
+        const float h[4] = {hi.x, hi.y, hi.z, hi.w}, l[4] = {lo.x, lo.y, lo.z, lo.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t off = ((uint32_t)(k >> 2) * Ko + 4 * n4 + e) * 16 + (k & 3) * 4;
+          *reinterpret_cast<float *>(wimg + off) = h[e];
+          *reinterpret_cast<float *>(wimg + wpart + off) = l[e];
+        }
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -329,9 +357,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int idx = e; idx < kM * q; idx += kEpi) {
           const int r = idx / q, ch = idx % q, sw = (ch & ~7) | ((ch ^ r) & 7);
           const int64_t grow = t * kM + r;
-          if (grow < a.n)
-            __stcs(reinterpret_cast<float4 *>(a.T + grow * a.ldt) + ch,
-                   *reinterpret_cast<const float4 *>(otile + ((size_t)r * q + sw) * 16));
+          if (grow < a.n) {
+            float4 v;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(smem_u32(otile + ((size_t)r * q + sw) * 16)));
+            __stcs(reinterpret_cast<float4 *>(a.T + grow * a.ldt) + ch, v);
+          }
         }
         asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
         continue;
@@ -350,6 +382,238 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&acce[b]);
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(a.tmem_cols));
+}
+
+// The direct form (default): the TMA's 128-B-swizzled X chunk IS the A
+// operand's hi part (kind::tf32 reads the fp32 bits and keeps the top 19:
+// hi = trunc(x)); the splitters only write lo = x - trunc(x), exact in fp32,
+// into the stage's second half in the same swizzled layout.  A stage is
+// [X chunk 16 KB (TMA) | lo 16 KB], freed by the MMA's commit, so every
+// stage's TMA is in flight with no separate raw ring.  (The dropped terms:
+// lo's own truncation and lo.lo, each < 2^-20 relative per product, inside
+// the c-1 bound.)
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_direct_kernel(const __grid_constant__ CUtensorMap xmap,
+                          const __grid_constant__ CUtensorMap tmap, const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int Ki = a.Ki, Ko = a.Ko, S = a.op_stages;
+  const uint32_t wpart = (uint32_t)Ki * Ko * 4;
+  uint8_t *stage0 = smem;                             // S x [X 16 KB | lo 16 KB]
+  uint8_t *wimg = stage0 + (size_t)S * kChunkBytes;   // [hi | lo], each [Ki/4][Ko][4]
+  uint8_t *otile = wimg + 2 * wpart;  // stage_out: 2 x [Ko/32 blocks of 128 rows x 128 B]
+  uint64_t *bar =
+      reinterpret_cast<uint64_t *>(otile + (a.stage_out ? 2 * (size_t)kM * Ko * 4 : 0));
+  uint64_t *xfull = bar, *lofull = bar + S, *empty = bar + 2 * S, *accf = bar + 3 * S,
+           *acce = bar + 3 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tiles = (a.n + kM - 1) / kM;
+  const int chunks = Ki / kKc;
+
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(a.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&lofull[s], kLoaders);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], kEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {  // W -> hi / lo image (as gemm_tc_kernel)
+    const int q = Ko / 4;
+    const int total = Ki * q;
+    for (int base = tid; base < total; base += kThreads * 8) {
+      float4 w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * kThreads;
+        w[u] = i < total ? __ldg(reinterpret_cast<const float4 *>(a.W + (int64_t)(i / q) * a.ldw +
+                                                                   4 * (i % q)))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * kThreads;
+        if (i >= total) break;
+        const int k = i / q, n4 = i % q;
+        float4 hi, lo;
+        split4(w[u], hi, lo);
+        const float h[4] = {hi.x, hi.y, hi.z, hi.w}, l[4] = {lo.x, lo.y, lo.z, lo.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t off = ((uint32_t)(k >> 2) * Ko + 4 * n4 + e) * 16 + (k & 3) * 4;
+          *reinterpret_cast<float *>(wimg + off) = h[e];
+          *reinterpret_cast<float *>(wimg + wpart + off) = l[e];
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 9) {  // TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x)
+        for (int c = 0; c < chunks; ++c, ++it) {
+          const int s = it % S;
+          if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+          mbar_expect_tx(&xfull[s], kChunkPart);
+          tma_2d(smem_u32(stage0 + (size_t)s * kChunkBytes), &xmap, &xfull[s], c * kKc,
+                 (int)(t * kM));
+        }
+    }
+    __syncwarp();
+  } else if (warp < 4) {  // splitters: lo = x - trunc(x), same swizzled position
+    int it = 0;
+    const uint32_t sw = (uint32_t)(tid & 7);
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int c = 0; c < chunks; ++c, ++it) {
+        const int s = it % S;
+        mbar_wait(&xfull[s], (it / S) & 1);
+        const uint32_t xr = smem_u32(stage0 + (size_t)s * kChunkBytes) + tid * 128;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const uint32_t o = ((g ^ sw) << 4);
+          uint4 x;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                       : "r"(xr + o));
+          const float4 lo = make_float4(
+              __uint_as_float(x.x) - __uint_as_float(x.x & 0xFFFFE000u),
+              __uint_as_float(x.y) - __uint_as_float(x.y & 0xFFFFE000u),
+              __uint_as_float(x.z) - __uint_as_float(x.z & 0xFFFFE000u),
+              __uint_as_float(x.w) - __uint_as_float(x.w & 0xFFFFE000u));
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(xr + kChunkPart + o),
+                       "f"(lo.x), "f"(lo.y), "f"(lo.z), "f"(lo.w)
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&lofull[s]);
+      }
+    }
+  } else if (warp == 4) {  // MMA issuer
+    if (lane == 0) {
+      const uint32_t id = idesc(Ko);
+      const uint32_t bytes_b = (uint32_t)Ko * 16;
+      const uint32_t whi = smem_u32(wimg), wlo = whi + wpart;
+      int it = 0, tl = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        const int b = tl & 1;
+        if (tl >= 2) mbar_wait(&acce[b], ((tl >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)(b * Ko);
+        for (int c = 0; c < chunks; ++c, ++it) {
+          const int s = it % S;
+          mbar_wait(&lofull[s], (it / S) & 1);  // the splitters saw xfull: X landed too
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t xhi = smem_u32(stage0 + (size_t)s * kChunkBytes), xlo = xhi + kChunkPart;
+#pragma unroll
+          for (int ks = 0; ks < kKc / 8; ++ks) {
+            const uint64_t dah = desc_sw128(xhi + ks * 32), dal = desc_sw128(xlo + ks * 32);
+            const uint32_t ob = (uint32_t)(c * (kKc / 4) + 2 * ks) * bytes_b;
+            const uint64_t dbh = desc(whi + ob, bytes_b, 128), dbl = desc(wlo + ob, bytes_b, 128);
+            mma_tf32(acc, dah, dbh, id, (c > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32(acc, dah, dbl, id, 1u);
+            mma_tf32(acc, dal, dbh, id, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&accf[b]);
+      }
+    }
+    __syncwarp();
+  } else {  // epilogue (warps 5-8), as gemm_tc_kernel
+    const int quarter = warp & 3;
+    int tl = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+      const int b = tl & 1;
+      mbar_wait(&accf[b], (tl >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int rloc = quarter * 32 + lane;
+      const int64_t row = t * kM + rloc;
+      const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * Ko);
+      if (a.stage_out) {
+        // TMEM -> shared tile in the TMA store's 128-B swizzle (32-column
+        // blocks of 128 rows x 128 B; chunk j of row r at j ^ (r % 8)), then
+        // one elected thread stores the tile with TMA tensor stores; two
+        // tile buffers, so a store drains while the next tile is staged
+        uint8_t *ot = otile + (size_t)(tl & 1) * kM * Ko * 4;
+        const bool leader = tid == kLoaders + 32;
+        if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+        for (int c0 = 0; c0 < Ko; c0 += 64) {
+          uint32_t v[4][16];
+          const int nc = Ko - c0 < 64 ? (Ko - c0) / 16 : 4;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < nc) tmem_ld16_nowait(tb + c0 + 16 * u, v[u]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < nc) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int col = c0 + 16 * u + 4 * j;  // first column of this 16-B chunk
+                const int blk = col >> 5, ch = (col & 31) >> 2;
+                const uint32_t addr = smem_u32(ot + (size_t)blk * kM * 128 + rloc * 128 +
+                                               ((ch ^ (rloc & 7)) << 4));
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+                             "r"(v[u][4 * j]), "r"(v[u][4 * j + 1]), "r"(v[u][4 * j + 2]),
+                             "r"(v[u][4 * j + 3])
+                             : "memory");
+              }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&acce[b]);  // TMEM buffer free: the next tile's MMAs may start
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+        if (leader) {
+          for (int blk = 0; blk < Ko / 32; ++blk)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmap)),
+                "r"(blk * 32), "r"((int)(t * kM)), "r"(smem_u32(ot + (size_t)blk * kM * 128))
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        continue;
+      }
+      for (int c = 0; c < Ko; c += 16) {
+        float v[16];
+        tmem_ld16(tb + c, v);
+        if (row < a.n) {
+          float4 *dst = reinterpret_cast<float4 *>(a.T + row * a.ldt + c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            __stcs(dst + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acce[b]);
+    }
+  }
+  if (a.stage_out && tid == kLoaders + 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 4)
@@ -411,8 +675,6 @@ pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     PSPMM_FAIL(PSPMM_ERR_CUDA, "dense_gemm: tensor map encode failed");
-  PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
   GemmArgs args;
   args.X = d_X;
   args.W = d_W;
@@ -429,6 +691,41 @@ pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_
   args.tmem_cols = tmem_cols_for(Ko);
   const int64_t tiles = (n + kM - 1) / kM;
   const int grid = (int)std::min<int64_t>(tiles, num_sms());
+  // the direct form (TMA chunk = hi operand, default) with as many 32-KB
+  // stages as fit (2..6); PSPMM_GEMM_DIRECT=0 (A/B knob) takes the raw-ring form
+  const char *de = std::getenv("PSPMM_GEMM_DIRECT");
+  if (!(de && de[0] == '0')) {
+    // the direct form's staged epilogue: two tile buffers written out by TMA
+    // tensor stores (Ko % 32 == 0)
+    bool so = !(se && se[0] == '0') && Ko % 32 == 0 &&
+              1024 + 512 + w + 2 * otile + 2ll * kChunkBytes <= kMaxSmem;
+    const int64_t base_d = 1024 + 512 + w + (so ? 2 * otile : 0);
+    int sd = (int)std::min<int64_t>(6, (kMaxSmem - base_d) / kChunkBytes);
+    if (const char *e = std::getenv("PSPMM_GEMM_OPS")) sd = std::max(2, std::min(sd, std::atoi(e)));
+    CUtensorMap tmapT;
+    if (so) {
+      cuuint64_t tdims[2] = {(cuuint64_t)Ko, (cuuint64_t)n};
+      cuuint64_t tstr[1] = {(cuuint64_t)ldt * 4};
+      cuuint32_t tbox[2] = {32, (cuuint32_t)kM};
+      if (encode(&tmapT, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d_T, tdims, tstr, tbox, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        so = false;
+    }
+    if (!so) std::memset(&tmapT, 0, sizeof(tmapT));
+    if (sd >= 2) {
+      args.op_stages = sd;
+      args.stage_out = so ? 1 : 0;
+      const size_t smem_d = (size_t)(base_d + (int64_t)sd * kChunkBytes);
+      PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_direct_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d));
+      gemm_tc_direct_kernel<<<grid, kThreads, smem_d, stream>>>(map, tmapT, args);
+      PSPMM_CUDA_TRY(cudaGetLastError());
+      return PSPMM_OK;
+    }
+  }
+  PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
   gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(map, args);
   PSPMM_CUDA_TRY(cudaGetLastError());
   return PSPMM_OK;
