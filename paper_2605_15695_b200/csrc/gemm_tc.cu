@@ -11,6 +11,9 @@
 // lo = rna(x - hi); X.W ~ Xhi.Whi + Xhi.Wlo + Xlo.Whi (the dropped lo.lo
 // term is below 2^-22 relative), accumulated in fp32 in TMEM.
 //
+// Default: gemm_tc_direct_kernel (below) — the TMA chunk is itself the A
+// operand's hi part, splitters write only lo, epilogue by TMA tensor stores.
+// gemm_tc_kernel (PSPMM_GEMM_DIRECT=0) is the raw-ring form described here.
 // One persistent CTA per SM, warp-specialised (10 warps):
 //  - warp 9 lane 0 (TMA): streams X in chunks of 128 rows x 32 columns
 //    (16 KB, one 2-D TMA copy, 128-B swizzle, rows past n zero-filled) into
