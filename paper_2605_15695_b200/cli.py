@@ -191,6 +191,11 @@ def cmd_spmm(a, api):
         d_rp, d_ci, d_val = _device_csr(rp, ci, val)
         A = api.pspmm_pcsr_build(n, int(rp[-1]), d_rp, d_ci, d_val, cfg.V, cfg.S, cfg.omega,
                                  cfg.sg_override, n_cols=nc)
+        if feats is not None:  # the library's engine rules, in bench.py's order
+            K = int(_B(a, nc).shape[1])
+            cfg, _ = api.auto_dense(A, d_rp, d_ci, d_val, K, cfg)
+            cfg, A, _ = api.auto_blocks(A, d_rp, d_ci, d_val, K, cfg)
+            cfg, A, _ = api.auto_band(A, d_rp, d_ci, d_val, K, cfg, feats)
     B = torch.from_numpy(_B(a, nc)).cuda()
     C = torch.empty((n, B.shape[1]), device="cuda")
     api.pspmm_spmm_run(A, B, C, cfg)
