@@ -441,10 +441,16 @@ pspmm_status pspmm_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz,
                                  float *d_t_val, void *stream);
 
 /*
- * (f3) Dense product of a GNN layer: T = X . W in fp32 (CUDA cores; the
- * skinny n x Ki by Ki x Ko product is HBM-bound).  X: n x Ki (ldx), W:
- * Ki x Ko (ldw), T: n x Ko (ldt), all row-major device fp32.  Ki <= 800.
- * Sequential fp32 accumulation over Ki.  Asynchronous on `stream`.
+ * (f3) Dense product of a GNN layer: T = X . W, fp32 in and out.  X: n x Ki
+ * (ldx), W: Ki x Ko (ldw), T: n x Ko (ldt), all row-major device fp32.
+ * When Ki % 32 == 0, Ko % 16 == 0, ld % 4 == 0 and X / W / T are 16-B
+ * aligned it runs on the tcgen05 tensor cores (kind::tf32 "3xTF32": x = hi
+ * + lo, Xhi.Whi + Xhi.Wlo + Xlo.Whi accumulated in fp32 in TMEM; the dropped
+ * terms are < 2^-20 relative per product), in output-column blocks of at
+ * most 256 when W's TF32 image does not fit shared memory whole; otherwise
+ * on CUDA cores with sequential fp32 accumulation over Ki (Ki <= 800, else
+ * PSPMM_ERR_UNSUPPORTED).  Both stay within 1e-5 sum |x||w| of the exact
+ * product.  Asynchronous on `stream`.
  */
 pspmm_status pspmm_dense_gemm(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
                               const float *d_W, int64_t ldw, float *d_T, int64_t ldt,

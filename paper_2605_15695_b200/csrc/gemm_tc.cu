@@ -635,21 +635,50 @@ int tmem_cols_for(int Ko) {
 // Shapes the tensor-core product takes: Ki % 32 == 0, Ko % 16 == 0,
 // 16 <= Ko <= 256, W's hi / lo image plus two X stages in shared memory,
 // 16-B aligned X / W / T with ld % 4 == 0.
+// Output-column block width so W's hi / lo image (Ki x Kob x 8 B) fits beside
+// two stages and N = Kob <= 256: Ko itself when it fits, else the widest
+// divisor of Ko that is a multiple of 16 and fits
+// (each block is then an independent launch over the same X: X re-streams).
+int gemm_tc_block(int32_t Ki, int32_t Ko) {
+  for (int b = std::min(Ko, 256); b >= 16; b -= 16) {  // MMA N <= 256, TMEM 2 x N <= 512
+    if (Ko % b != 0) continue;
+    if (2ll * Ki * b * 4 + 2ll * kChunkBytes + 2ll * kRawBytes + 1024 + 512 <= kMaxSmem) return b;
+  }
+  return 0;
+}
+
 bool gemm_tc_supported(int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx, const float *d_W,
                        int64_t ldw, const float *d_T, int64_t ldt) {
-  if (Ki < kKc || Ki % kKc != 0 || Ko < 16 || Ko > 256 || Ko % 16 != 0) return false;
+  if (Ki < kKc || Ki % kKc != 0 || Ko < 16 || Ko % 16 != 0) return false;
+  if (gemm_tc_block(Ki, Ko) == 0) return false;
   if (ldx % 4 || ldw % 4 || ldt % 4) return false;
   if ((reinterpret_cast<uintptr_t>(d_X) | reinterpret_cast<uintptr_t>(d_W) |
        reinterpret_cast<uintptr_t>(d_T)) & 15)
     return false;
   if (!tensor_map_encoder()) return false;
-  const int64_t w = 2ll * Ki * Ko * 4;
-  return w + 2ll * kChunkBytes + 2ll * kRawBytes + 1024 + 512 <= kMaxSmem;  // >= 2 + 2 stages
+  return true;
 }
+
+pspmm_status gemm_tc_one(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
+                         const float *d_W, int64_t ldw, float *d_T, int64_t ldt,
+                         cudaStream_t stream);
 
 pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
                      const float *d_W, int64_t ldw, float *d_T, int64_t ldt, cudaStream_t stream) {
   if (n == 0) return PSPMM_OK;
+  const int b = gemm_tc_block(Ki, Ko);
+  if (b <= 0) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "dense_gemm: no tensor-core column block fits");
+  for (int j0 = 0; j0 < Ko; j0 += b) {  // T[:, j0:j0+b] = X . W[:, j0:j0+b]
+    pspmm_status st = gemm_tc_one(n, Ki, std::min(b, Ko - j0), d_X, ldx, d_W + j0, ldw, d_T + j0,
+                                  ldt, stream);
+    if (st != PSPMM_OK) return st;
+  }
+  return PSPMM_OK;
+}
+
+pspmm_status gemm_tc_one(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
+                         const float *d_W, int64_t ldw, float *d_T, int64_t ldt,
+                         cudaStream_t stream) {
   if (n > 0x7fffffffll) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "dense_gemm: n >= 2^31");
   const int64_t w = 2ll * Ki * Ko * 4;
   // the staged epilogue (coalesced row stores) when its tile fits beside two

@@ -10,7 +10,7 @@
 // byte a block needs moves by bulk copy, issued from one descriptor:
 //
 //  - pack (pspmm_pcsr_attach_band, once per graph): rows in blocks of R =
-//    64 / 32 / 16 rows (k_max <= 32 / 64 / 128, so the band of a lattice
+//    128 / 64 / 32 / 16 rows (k_max <= 16 / 32 / 64 / 128, so the band of a lattice
 //    block fits the budget at any K); per block a descriptor {first range,
 //    ranges, first nonzero, end nonzero} and its staged-row count; per range
 //    {first B row, rows, slot in the band}, where a range is a run of the
@@ -46,14 +46,17 @@ constexpr int kThreads = 128;
 constexpr int kGap = 8;              // merge column ranges separated by <= kGap rows
 constexpr int kPairCap = 512;        // pairs staged per block (4 KB); more: read from global
 
-int block_rows(int k_max) { return k_max <= 32 ? 64 : k_max <= 64 ? 32 : 16; }
+constexpr int kMaxRows = 128;  // rows per block at most (the stage's rowPtr slice)
+int block_rows(int k_max) {
+  return k_max <= 16 ? 128 : k_max <= 32 ? 64 : k_max <= 64 ? 32 : 16;
+}
 
 struct BandArgs {
   const int4 *__restrict__ desc;        // blocks: {first range, ranges, p0, p1}
   const int32_t *__restrict__ staged;   // blocks: staged band rows (-1: over budget)
   const int4 *__restrict__ rng;         // ranges: {first B row, rows, band slot, 0}
   const int2 *__restrict__ pairs;       // nnz (+2 pad): (slot or column, value bits)
-  const int32_t *__restrict__ rowptr;   // padded copy (n + 1 + 64)
+  const int32_t *__restrict__ rowptr;   // padded copy (n + 1 + kMaxRows)
   const float *__restrict__ B;
   float *__restrict__ C;
   int64_t ldb, ldc;
@@ -104,7 +107,7 @@ __device__ __forceinline__ void fma4(float4 &acc, float v, const float4 &b) {
 // stages, so the next block's copies are in flight while this one computes.
 constexpr int kMaxStages = 4;
 constexpr int kRPG = 4;  // rows per row group in one block (R = kRPG x 128 / G at K = 4 G)
-constexpr int kStageBytes = kBandBytes + kPairCap * 8 + 64 * 4 + 32;  // + info
+constexpr int kStageBytes = kBandBytes + kPairCap * 8 + kMaxRows * 4 + 32;  // + info
 
 template <int G>
 __global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandArgs a) {
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandA
       const int4 dn = nb < nblk ? a.desc[nb] : make_int4(0, 0, 0, 0);
       const int stn = nb < nblk ? a.staged[nb] : 0;
       unsigned char *st = smem + s * kStageBytes;
-      int *info = reinterpret_cast<int *>(st + kBandBytes + kPairCap * 8 + 64 * 4);
+      int *info = reinterpret_cast<int *>(st + kBandBytes + kPairCap * 8 + kMaxRows * 4);
       const int64_t r0 = blk * a.R;
       const int rows = (int)(a.n_rows - r0 < a.R ? a.n_rows - r0 : a.R);
       const int pb = d.z & ~1, pcnt = (d.w - pb + 1) & ~1;  // 16-B aligned pair run
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kThreads + 32, 3) spmm_band_kernel(const BandA
     unsigned char *st = smem + s * kStageBytes;
     const int2 *spairs = reinterpret_cast<const int2 *>(st + kBandBytes);
     const int32_t *srp = reinterpret_cast<const int32_t *>(st + kBandBytes + kPairCap * 8);
-    const int *info = reinterpret_cast<const int *>(st + kBandBytes + kPairCap * 8 + 64 * 4);
+    const int *info = reinterpret_cast<const int *>(st + kBandBytes + kPairCap * 8 + kMaxRows * 4);
     mbar_wait_parity(&full[s], (it / S) & 1);
     const int staged = info[0], pb = info[1], p_end = info[2], rows = info[3];
     const int64_t r0 = blk * a.R;
@@ -321,10 +324,10 @@ pspmm_status attach_band(pspmm_pcsr_s *A, int32_t k_max, cudaStream_t stream, do
   const int64_t nblk = (n + R - 1) / R;
   const int64_t max_rows = kBandBytes / ((int64_t)k_max * 4);  // staged rows per block
   PSPMM_CUDA_TRY(cudaStreamSynchronize(stream));
-  std::vector<int32_t> rp(n + 1 + 64), ci(nnz);
+  std::vector<int32_t> rp(n + 1 + kMaxRows), ci(nnz);
   std::vector<float> vl(nnz);
   PSPMM_CUDA_TRY(cudaMemcpy(rp.data(), A->d_rowptr, (n + 1) * 4, cudaMemcpyDeviceToHost));
-  for (int k = 0; k < 64; ++k) rp[n + 1 + k] = rp[n];
+  for (int k = 0; k < kMaxRows; ++k) rp[n + 1 + k] = rp[n];
   if (nnz) {
     PSPMM_CUDA_TRY(cudaMemcpy(ci.data(), A->d_colidx, nnz * 4, cudaMemcpyDeviceToHost));
     PSPMM_CUDA_TRY(cudaMemcpy(vl.data(), A->d_val, nnz * 4, cudaMemcpyDeviceToHost));

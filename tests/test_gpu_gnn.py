@@ -38,10 +38,12 @@ def test_dense_gemm(n, Ki, Ko):
 @pytest.mark.parametrize("n,Ki,Ko,pad", [(1, 32, 16, 0), (127, 64, 64, 0), (128, 64, 64, 0),
                                          (129, 64, 64, 4), (1000, 128, 128, 0),
                                          (4097, 256, 64, 0), (3000, 64, 256, 8),
-                                         (20000, 32, 48, 0), (300, 96, 112, 0)])
+                                         (20000, 32, 48, 0), (300, 96, 112, 0),
+                                         (1000, 256, 256, 0), (777, 64, 512, 4)])
 def test_dense_gemm_tensor_core_shapes(n, Ki, Ko, pad, force_cc, monkeypatch):
-    """Shapes the tcgen05 3xTF32 product takes (gemm_tc.cu: Ki % 32, Ko % 16,
-    Ko <= 256), ragged tiles (n % 128 != 0), padded leading dimensions; the
+    """Shapes the tcgen05 3xTF32 product takes (gemm_tc.cu: Ki % 32, Ko % 16;
+    W's image in column blocks when it is too large: 256 x 256, 64 x 512),
+    ragged tiles (n % 128 != 0), padded leading dimensions; the
     same shapes forced onto the CUDA-core kernel (PSPMM_GEMM_CC=1).  Both
     against the fp64 product with the c-1 bound on |X| |W|."""
     import torch
