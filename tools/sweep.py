@@ -45,7 +45,9 @@ def lattice(K, Ws=(2, 4, 8), max_passes=16):
     return out
 
 
-def corpus_graphs(count, seed=12345, n_lo=20000, n_hi=400000, prefix=""):
+def corpus_graphs(count, seed=12345, n_lo=20000, n_hi=400000, prefix="",
+                  kinds=("powerlaw", "uniform", "banded", "community", "chung_lu",
+                         "community_shuffled"), d_range=None):
     """Synthetic graphs across generators, exponents and ID orders (decider
     training corpus; n ~ 2e4 .. 4e5 by default; the round-2 supplements use
     n ~ 1e3 .. 2e4 and 8e5 .. 3e6 so the bench graphs' sizes are inside the
@@ -54,12 +56,13 @@ def corpus_graphs(count, seed=12345, n_lo=20000, n_hi=400000, prefix=""):
     rng = np.random.default_rng(seed)
     gs = []
     for i in range(count):
-        kind = ["powerlaw", "uniform", "banded", "community", "chung_lu", "community_shuffled"][i % 6]
+        kind = kinds[i % len(kinds)]
         n = int(np.exp(rng.uniform(np.log(n_lo), np.log(n_hi)))) if n_lo < 20000 or \
             n_hi > 400000 else int(rng.integers(n_lo, n_hi))
         s = int(rng.integers(1, 1 << 30))
         if kind == "powerlaw":
-            g = gen.powerlaw(n, float(rng.uniform(4, 64)), float(rng.uniform(1.8, 3.0)), s)
+            g = gen.powerlaw(n, float(rng.uniform(*(d_range or (4, 64)))),
+                             float(rng.uniform(1.8, 3.0)), s)
         elif kind == "uniform":
             g = gen.uniform(n, float(rng.uniform(2, 48)), s)
         elif kind == "banded":
@@ -68,7 +71,8 @@ def corpus_graphs(count, seed=12345, n_lo=20000, n_hi=400000, prefix=""):
             g = gen.community(n, int(rng.choice([32, 128, 512, 2048])), float(rng.uniform(4, 64)),
                               float(rng.uniform(0.5, 0.95)), s, ordered=(kind == "community"))
         else:
-            d = float(min(rng.uniform(4, 200), 2e7 / n, max(4.0, n / 8.0)))  # nnz <= 2e7
+            d = float(min(rng.uniform(*(d_range or (4, 200))), 2e7 / n,
+                          max(4.0, n / 8.0)))  # nnz <= 2e7
             nnz = int(n * d) // 2 * 2
             rp, ci = gen.chung_lu(n, nnz, int(min(n - 1, d * rng.uniform(10, 60))), s,
                                   shuffle_seed=s + 1)
@@ -207,6 +211,9 @@ def main():
     ap.add_argument("--corpus-seed", type=int, default=12345)
     ap.add_argument("--corpus-n", default="20000,400000", help="node-count range lo,hi")
     ap.add_argument("--corpus-prefix", default="")
+    ap.add_argument("--corpus-d", default="", help="mean-degree range lo,hi (power law, Chung-Lu)")
+    ap.add_argument("--corpus-kinds", default="",
+                    help="comma list of generators to cycle (default: all six)")
     ap.add_argument("--Ks", default="")
     ap.add_argument("--iters", type=int, default=7)
     ap.add_argument("--Ws", default="2,4,8")
@@ -278,7 +285,10 @@ def main():
     if a.corpus:
         Ks = [int(k) for k in a.Ks.split(",")] if a.Ks else [16, 32, 64, 128, 256]
         lo, hi = (int(x) for x in a.corpus_n.split(","))
-        for g in corpus_graphs(a.corpus, a.corpus_seed, lo, hi, a.corpus_prefix):
+        kinds = tuple(a.corpus_kinds.split(",")) if a.corpus_kinds else (
+            "powerlaw", "uniform", "banded", "community", "chung_lu", "community_shuffled")
+        d_range = tuple(float(x) for x in a.corpus_d.split(",")) if a.corpus_d else None
+        for g in corpus_graphs(a.corpus, a.corpus_seed, lo, hi, a.corpus_prefix, kinds, d_range):
             recs += sweep_graph(g, Ks, a.iters, flush, stream, Ws, VS, modes, orders, cands)
             print(f"[{time.time() - t0:.0f}s] {g.name} n={g.n} nnz={g.nnz}", flush=True)
             json.dump(recs, open(a.out, "w"))
