@@ -310,7 +310,8 @@ pspmm_status pspmm_block_info(pspmm_pcsr A, int32_t *block_rows, int64_t *window
 /*
  * (a6 on locality-ordered graphs: the paper's reordering step, P:271-272
  * §4.4, and its locality argument for blocking) Engine mode 6:
- * staged bands.  Rows are grouped in blocks of 128; each block's distinct
+ * staged bands.  Rows are grouped in blocks of 128 / 64 / 32 / 16 rows
+ * (k_max <= 16 / 32 / 64 / 128); each block's distinct
  * columns are merged into contiguous ranges of B rows (gaps of <= 8 rows
  * included), and a CTA stages the whole band with one 1-D bulk copy per
  * range into shared memory before any row is computed, while its rows'
@@ -322,7 +323,7 @@ pspmm_status pspmm_block_info(pspmm_pcsr A, int32_t *block_rows, int64_t *window
  * uploaded; 4 B per nonzero + 8 B per range): per block the ranges and each
  * nonzero's row slot in the band.  k_max (multiple of 4, 4..128) bounds the
  * K and the B row pitch (ldb) of later runs: a block is staged when its band
- * fits 64 KB at k_max columns; other blocks keep the column and gather from
+ * fits 32 KB at k_max columns; other blocks keep the column and gather from
  * global memory.  *staged_frac (may be NULL) = staged / non-empty blocks.
  * Replaces a previous pack; freed by pspmm_pcsr_destroy.  Synchronises
  * `stream`.  UNSUPPORTED unless V = 1, S = 0; INVALID_ARG for a bad k_max.

@@ -57,7 +57,7 @@ struct RowBlocks {
   int2 *d_pairs = nullptr;         // (column - window start, value bits), windows padded to even
   int16_t *d_rowmap = nullptr;     // num_blocks x nw x rw: local row of a slot, -1 = none
 };
-// Engine mode 6 (spmm_band.cu): rows in blocks of 64 / 32 / 16 (by k_max);
+// Engine mode 6 (spmm_band.cu): rows in blocks of 128 / 64 / 32 / 16 (by k_max);
 // per block a descriptor, the contiguous ranges of B rows it touches (staged
 // by bulk copies) and every nonzero's (band slot, value) pair, attached by
 // pspmm_pcsr_attach_band.  Derived data, not part of the PCSR contract.
