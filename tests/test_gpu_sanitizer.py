@@ -22,6 +22,10 @@ def test_compute_sanitizer(tool):
                         sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")],
                        cwd=ROOT, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        # the GPU pool's compute-sanitizer wrapper refuses every run (exit 86):
+        # runs under it have left GPUs needing a reset; nothing ran
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert r.returncode == 0, out[-4000:]
     assert "sanitize run ok" in out
     # memcheck / synccheck: "ERROR SUMMARY: 0 errors"; racecheck:
