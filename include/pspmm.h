@@ -73,9 +73,8 @@ typedef enum {
  *     aligned B and C, else PSPMM_ERR_UNSUPPORTED; only W applies);
  *     3 = short-row pipeline for low-degree graphs (V = 1, S = 0, F in
  *     {1, 2, 4}, 128-bit layout; W, F, G apply);
- *     4 = short-row stream with cp.async shared-memory rings: a row group
- *     owns a contiguous row range and streams its vectors, B rows of 3
- *     batches ahead in flight (same constraints as 3; W, F, G apply);
+ *     (4: retired in round 2 -- a cp.async short-row stream that was slower
+ *     than mode 3 on every workload and never selected; PSPMM_ERR_UNSUPPORTED)
  *     5 = row blocks with shared-memory B reuse (pspmm_pcsr_attach_blocks;
  *     V = 1, S = 0, K % 128 == 0; W, F, G, order do not apply);
  *     1 = dense-panel tensor-core path: the dense 128 x 32 tiles attached by
@@ -405,7 +404,7 @@ pspmm_status pspmm_spmm_run_fanout(pspmm_pcsr A, const float *d_B, int64_t ldb, 
  * offset in the buffer).  The switch delivers the value to every bound copy,
  * d_C's own memory included, so no separate local store and no per-peer
  * unicast stores are issued.  d_C is read only when the engine needs C's old
- * value (never for C = A.B).  Engine modes 0, 3, 5 and 6 (mode 1, 2, 4:
+ * value (never for C = A.B).  Engine modes 0, 3, 5 and 6 (mode 1, 2:
  * PSPMM_ERR_UNSUPPORTED); same fences and barrier contract as
  * pspmm_spmm_run_fanout.  INVALID_ARG for a null d_C_mc or an alignment
  * differing from d_C's.  Asynchronous.

@@ -246,12 +246,6 @@ bool short_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc,
 pspmm_status run_spmm_short(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
                             float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
                             int64_t u0, int64_t u1, int32_t accumulate, const Fanout &fan);
-// spmm_async.cu (engine mode 4)
-bool async_supported(const pspmm_pcsr_s *A, int32_t K, int64_t ldb, int64_t ldc, const float *d_B,
-                     const float *d_C, const pspmm_config &cfg);
-pspmm_status run_spmm_async(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int32_t K,
-                            float *d_C, int64_t ldc, const pspmm_config &cfg, cudaStream_t stream,
-                            int64_t u0, int64_t u1, int32_t accumulate, const Fanout &fan);
 // host entry: H2D(B), engine in kSlices unit slices, D2H of each slice's C
 // rows on a second stream as soon as the slice is done
 pspmm_status run_spmm_host(pspmm_pcsr_s *A, const float *h_B, int64_t ldb, int32_t K, float *h_C,

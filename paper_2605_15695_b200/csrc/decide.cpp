@@ -97,12 +97,12 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
     c.W = lab[3];
     c.order = c.mode == 0 ? lab[6] : 0;
     if (c.mode == 2 && K % 32 != 0) c.mode = 0;  // TMA engine needs K % 32 == 0
-    if ((c.mode == 3 || c.mode == 4) && K % 4 != 0) c.mode = 0;  // short-row engines: 128-bit only
+    if (c.mode == 3 && K % 4 != 0) c.mode = 0;  // short-row engines: 128-bit only
     // the short-row engines walk a row's vectors beyond the staged window one
     // dependent load at a time: a hub row serialises its group (K sweep,
     // Cora K = 128, mode 3 0.059 ms vs cuSPARSE 0.023), so
     // graphs with rows longer than 64 vectors stay on mode 0
-    if ((c.mode == 3 || c.mode == 4) && f->d_max > 64.0) c.mode = 0;
+    if (c.mode == 3 && f->d_max > 64.0) c.mode = 0;
     // vectorized blocking only where it saves B reads: at PR_2 ~ 0.5 a V = 2
     // vector is a padded single value (the paper's T1: V = 2 loses
     // at PR 47.8-49 %); the forest's V = 2 there extrapolates a noise-level

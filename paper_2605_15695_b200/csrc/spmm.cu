@@ -81,11 +81,10 @@ pspmm_status make_plan(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int
     PSPMM_FAIL(PSPMM_ERR_DIM_MISMATCH, "spmm_run: need K >= 1, ldb >= K, ldc >= K");
   if (cfg.V != A->V || cfg.S != A->S || cfg.omega != A->omega)
     PSPMM_FAIL(PSPMM_ERR_CONFIG_MISMATCH, "spmm_run: cfg.V/S/omega differ from the PCSR handle");
-  if (cfg.mode != 0 && cfg.mode != 2 && cfg.mode != 3 && cfg.mode != 4)
+  if (cfg.mode != 0 && cfg.mode != 2 && cfg.mode != 3)
     PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
-               "spmm_run: mode must be 0 (LDG engine), 1 (dense tiles on tensor cores; "
-               "pspmm_spmm_run / accumulate only), 2 (TMA gather), 3 (short rows) or 4 "
-               "(async-copy short rows)");
+               "spmm_run: mode must be 0 (LDG engine), 1 (dense tiles on tensor cores), "
+               "2 (TMA gather), 3 (short rows), 5 (row blocks) or 6 (staged bands)");
   if (!(cfg.W == 1 || cfg.W == 2 || cfg.W == 4 || cfg.W == 8))
     PSPMM_FAIL(PSPMM_ERR_CONFIG, "spmm_run: W must be 1, 2, 4 or 8");
   if (cfg.W * 32 > PSPMM_MAX_THREADS)
@@ -107,13 +106,6 @@ pspmm_status make_plan(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int
     if (!short_supported(A, K, ldb, ldc, d_B, d_C, cfg))
       PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
                  "spmm_run mode 3: needs V = 1, S = 0, F in {1, 2, 4}, K and ld % 4 == 0, "
-                 "16-B aligned B and C");
-    return PSPMM_OK;
-  }
-  if (cfg.mode == 4) {
-    if (!async_supported(A, K, ldb, ldc, d_B, d_C, cfg))
-      PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
-                 "spmm_run mode 4: needs V = 1, S = 0, F in {1, 2, 4}, K and ld % 4 == 0, "
                  "16-B aligned B and C");
     return PSPMM_OK;
   }
@@ -175,8 +167,6 @@ pspmm_status launch_range(const pspmm_pcsr_s *A, const Plan &plan, const float *
     return run_spmm_tma(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate, fan);
   if (cfg.mode == 3)
     return run_spmm_short(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate, fan);
-  if (cfg.mode == 4)
-    return run_spmm_async(A, d_B, ldb, K, d_C, ldc, cfg, stream, u0, u1, accumulate, fan);
   SpmmArgs args;
   args.rowptr = A->d_rowptr;
   args.colidx = A->d_colidx;
@@ -242,7 +232,7 @@ pspmm_status run_spmm(const pspmm_pcsr_s *A, const float *d_B, int64_t ldb, int3
     }
     if (fan->mc && fan->n != 1)
       PSPMM_FAIL(PSPMM_ERR_INVALID_ARG, "spmm_run_multicast: exactly one multicast address");
-    if (fan->mc && (cfg.mode == 2 || cfg.mode == 4))
+    if (fan->mc && cfg.mode == 2)
       PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED,
                  "spmm_run_multicast: engine modes 0, 3, 5 and 6 take the multicast epilogue");
     f = *fan;

@@ -62,7 +62,7 @@ def test_decider_returns_valid_config(K):
         assert c.V in (1, 2) and c.S in (0, 1) and c.W in (1, 2, 4, 8)
         assert 1 <= c.F <= 8 and c.G in (1, 2, 4, 8, 16, 32) and c.omega == 32
         assert c.mode == 0 or (c.mode == 2 and K % 32 == 0) or (
-            c.mode in (3, 4) and K % 4 == 0 and c.V == 1 and c.S == 0)
+            c.mode == 3 and K % 4 == 0 and c.V == 1 and c.S == 0)
         # pure: same input, same output
         assert api.pspmm_decide_config(dict(FEATS, pr2=pr2, d_max=dmax), K).as_dict() == c.as_dict()
 

@@ -74,7 +74,7 @@ def test_c_decider_evaluates_the_header_tree():
                  pr2=rng.uniform(0, 0.5))
         K = int(rng.choice([8, 16, 32, 48, 64, 96, 128, 160, 256]))
         mode, V, S, W, F, P, order = walk(model, f, K)
-        if mode in (3, 4) and f["d_max"] > 64:  # hub-row guard (decide.cpp)
+        if mode == 3 and f["d_max"] > 64:  # hub-row guard (decide.cpp)
             mode = 0
         if V == 2 and f["pr2"] >= 0.45:  # padding guard (decide.cpp)
             V = 1
@@ -87,7 +87,7 @@ def test_c_decider_evaluates_the_header_tree():
             G = ceil_pow2(-(-q // F))
         if mode == 2 and K % 32 == 0:
             assert (c.mode, c.V, c.S, c.W) == (2, V, S, W)
-        elif mode in (3, 4) and K % 4 == 0:
+        elif mode == 3 and K % 4 == 0:
             assert (c.mode, c.V, c.S, c.W, c.F) == (mode, V, S, W, F)
         else:
             assert (c.mode, c.V, c.S, c.W) == (0, V, S, W)

@@ -21,9 +21,9 @@ K = 64
 
 def _cases():
     out = []
-    for mode in (0, 2, 3, 4):
+    for mode in (0, 2, 3):
         for V, S in ((1, 0), (1, 1), (2, 0), (2, 1)):
-            if mode in (3, 4) and (V, S) != (1, 0):
+            if mode == 3 and (V, S) != (1, 0):
                 continue
             out.append((mode, V, S))
     return out

@@ -124,30 +124,25 @@ def test_tma_gather_engine(V, S, K, W):
     assert_parity(C, ref, mag, f"tma V{V} S{S} K{K} W{W}")
 
 
-@pytest.mark.parametrize("mode", [3, 4])
+@pytest.mark.parametrize("mode", [3])
 @pytest.mark.parametrize("name", ["roadnet_s", "cora", "giant", "banded", "reddit_s",
                                   "empty_rows"])
 @pytest.mark.parametrize("K", [16, 32, 64, 128, 160])
 @pytest.mark.parametrize("F", [1, 2, 4])
 def test_short_row_engines(mode, name, K, F):
-    """Engine modes 3 and 4 (V = 1, S = 0): rows of any length (mode 3's
-    inner window loop; mode 4's vector stream across row and sub-tile
-    boundaries, empty leading / trailing rows), every (F, G) the dispatcher
-    can pick, several column passes (K = 160)."""
+    """Engine mode 3 (V = 1, S = 0): rows of any length (the inner window
+    loop), every (F, G) the dispatcher can pick, several column passes
+    (K = 160)."""
     api = _api()
     g = graph(name)
     B = gen.dense(g.n, K, 500 + K)
     ref, mag = oracle_ref(g, B, key=(name, K, "short"))
     for W in (2, 8):
-        try:
-            C, _ = run(g, B, api.Config(W=W, F=F, V=1, S=0, mode=mode))
-        except api.PspmmError as e:  # mode 4: W warps' rings exceed shared memory
-            assert mode == 4 and F == 4 and W == 8 and e.status == api.PSPMM_ERR_CONFIG
-            continue
+        C, _ = run(g, B, api.Config(W=W, F=F, V=1, S=0, mode=mode))
         assert_parity(C, ref, mag, f"mode {mode} {name} K{K} F{F} W{W}")
 
 
-@pytest.mark.parametrize("mode", [3, 4])
+@pytest.mark.parametrize("mode", [3])
 def test_short_row_engine_rejects_other_corners(mode):
     api = _api()
     g = graph("cora")
@@ -158,10 +153,21 @@ def test_short_row_engine_rejects_other_corners(mode):
         assert e.value.status == api.PSPMM_ERR_UNSUPPORTED
 
 
+def test_retired_mode_4_rejected():
+    """Mode 4 (a cp.async short-row stream, never selected) was retired in
+    round 2: the engine reports it as an unsupported mode."""
+    api = _api()
+    g = graph("cora")
+    B = gen.dense(g.n, 16, 1)
+    with pytest.raises(api.PspmmError) as e:
+        run(g, B, api.Config(W=4, F=1, V=1, S=0, mode=4))
+    assert e.value.status == api.PSPMM_ERR_UNSUPPORTED
+
+
 @pytest.mark.parametrize("rows", [1, 2, 31, 32, 33, 64, 65, 1000])
-def test_async_engine_tiny_and_sub_tile_edges(rows):
-    """Mode 4 with fewer rows than groups and row counts at the 32-row
-    sub-tile boundaries (rowPtr staging), including all-empty matrices."""
+def test_short_row_engine_tiny_edges(rows):
+    """Mode 3 with fewer rows than groups and row counts around warp
+    multiples, including all-empty matrices."""
     api = _api()
     for density in (0.0, 3.0):
         g = gen.uniform(rows, density, 7) if density else gen.Graph(
@@ -169,8 +175,8 @@ def test_async_engine_tiny_and_sub_tile_edges(rows):
             np.zeros(0, np.float32))
         B = gen.dense(g.n, 32, 9)
         ref, mag = oracle_ref(g, B)
-        C, _ = run(g, B, api.Config(W=4, F=1, V=1, S=0, mode=4))
-        assert_parity(C, ref, mag, f"async rows {rows} d {density}")
+        C, _ = run(g, B, api.Config(W=4, F=1, V=1, S=0, mode=3))
+        assert_parity(C, ref, mag, f"short rows {rows} d {density}")
 
 
 def test_tma_engine_rejects_unsupported_K():

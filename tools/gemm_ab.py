@@ -61,19 +61,19 @@ def main():
     X = torch.rand((n, 64), device="cuda") * 2 - 1
     W = torch.rand((64, 64), device="cuda") * 2 - 1
     T = torch.empty((n, 64), device="cuda")
-    for ops in ("2", "3", "4"):
-        for so in ("1", "0"):
-            os.environ["PSPMM_GEMM_OPS"], os.environ["PSPMM_GEMM_STAGE_OUT"] = ops, so
+    for ops in ("2", "4", "8"):
+        for so in ("2", "0"):
+            os.environ["PSPMM_GEMM_XS"], os.environ["PSPMM_GEMM_OB"] = ops, so
             with torch.cuda.stream(stream):
                 step = lambda: api.pspmm_dense_gemm(X, W, T, stream)
                 cold = bench.time_steps(step, a.iters, 3, flush, stream)
             torch.cuda.synchronize()
-            rec = {"variant": f"ops{ops}_stageout{so}", "cold_ms": float(np.median(cold)),
+            rec = {"variant": f"xs{ops}_ob{so}", "cold_ms": float(np.median(cold)),
                    "cold_gbs": 4 * n * 128 / (np.median(cold) * 1e-3) / 1e9}
             print(json.dumps(rec), flush=True)
             out.write(json.dumps(rec) + "\n")
-    os.environ.pop("PSPMM_GEMM_OPS")
-    os.environ.pop("PSPMM_GEMM_STAGE_OUT")
+    os.environ.pop("PSPMM_GEMM_XS")
+    os.environ.pop("PSPMM_GEMM_OB")
     # the layer on Reddit: Y = A (X W) with Ki = Ko = 64 vs the SpMM alone
     g = bench.load_graph("reddit")
     rp, ci, vl = (torch.from_numpy(x).cuda() for x in (g.rowptr, g.colidx, g.val))

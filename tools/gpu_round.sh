@@ -65,16 +65,9 @@ if want sweep_order; then
       --orders 1 --out $O/sweep_corpus_o1.json > $O/sweep_corpus_o1.log 2>&1
 fi
 if want tests4; then
-  timeout 1800 python -m pytest tests -m gpu -q -k "short or async or fanout or accumulate or cli or host" \
+  timeout 1800 python -m pytest tests -m gpu -q -k "short or fanout or accumulate or cli or host" \
       --maxfail=10 > $O/pytest_gpu4.log 2>&1
   echo "pytest exit $?" >> $O/pytest_gpu4.log
-fi
-if want sweep4; then
-  # engine mode 4 (V = 1, S = 0 only), merged by (graph, K) like mode 3
-  timeout 900 python tools/sweep.py --workloads cora,roadnet,reddit,proteins,products --iters 5 \
-      --VS 10 --modes 3,4 --out $O/sweep_workloads_m4.json > $O/sweep_workloads_m4.log 2>&1
-  timeout 1800 python tools/sweep.py --corpus 60 --Ks 16,32,64,128,256 --iters 5 --VS 10 \
-      --modes 4 --out $O/sweep_corpus_m4.json > $O/sweep_corpus_m4.log 2>&1
 fi
 if want quickbench; then
   timeout 900 python bench.py --headline-only > $O/bench_quick.log 2>&1
@@ -87,23 +80,6 @@ if want rehearse; then
         --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 4 --warmup 3 \
         --dist-backend gloo --exchange $ex --workload reddit > $O/rehearse_$ex.log 2>&1
     echo "exit $?" >> $O/rehearse_$ex.log
-  done
-fi
-if want async_ab; then
-  for v in main ad2 ad6 au8 ad6u8; do
-    if [ "$v" = main ]; then unset PSPMM_LIB; M=3,4; else export PSPMM_LIB=$PWD/paper_2605_15695_b200/variants/libpspmm_$v.so; M=4; fi
-    timeout 600 python tools/sweep.py --workloads roadnet,cora --VS 10 --modes $M --Ws 2,4,8 --iters 7 \
-        --out $O/async_$v.json > $O/async_$v.log 2>&1
-  done
-  unset PSPMM_LIB
-  for m in 3 4; do
-    if [ $m = 3 ]; then X="--W 2 --F 2 --G 4"; else X="--W 8 --F 1 --G 8"; fi
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm -s 1 -c 1 \
-        -o /tmp/prof_rn_m$m -f python tools/run_kernel.py --workload roadnet --iters 2 --V 1 --S 0 \
-        --mode $m $X > $O/ncu_rn_m$m.log 2>&1
-    python tools/ncu_summary.py /tmp/prof_rn_m$m.ncu-rep --json $O/ncu_rn_m$m.json > /dev/null 2>&1
-    ncu -i /tmp/prof_rn_m$m.ncu-rep --page source --csv > $O/ncu_rn_m${m}_source.csv 2>/dev/null
-    ncu -i /tmp/prof_rn_m$m.ncu-rep --page details --csv > $O/ncu_rn_m${m}_details.csv 2>/dev/null
   done
 fi
 if want short_ab; then

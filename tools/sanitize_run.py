@@ -1,6 +1,6 @@
 """Tiny end-to-end run of every native kernel for compute-sanitizer
 (tests/test_gpu_sanitizer.py): CSR validation, features, the PCSR builder
-(V x S corners), engine modes 0 / 2 / 3 / 4, mode 1 (dense-tile split,
+(V x S corners), engine modes 0 / 2 / 3, mode 1 (dense-tile split,
 split_b_kernel, dense_tc_kernel), mode 5 (row blocks: touched-window metric,
 TMA-staged windows), mode 6 (staged bands, staged and global blocks), the
 fan-out epilogue (peer stores), the transpose, the permutation kernels and
@@ -30,14 +30,14 @@ def main():
             for S in (0, 1):
                 A = api.pspmm_pcsr_build(g.n, g.nnz, rp, ci, vl, V, S, 32, 16 if S else 0)
                 cfg = api.pspmm_decide_config(f, K)
-                for mode in (0, 2, 3, 4):
+                for mode in (0, 2, 3):
                     if mode == 2 and K % 32:
                         continue
-                    if mode in (3, 4) and (V, S) != (1, 0) or mode in (3, 4) and K % 4:
+                    if mode == 3 and (V, S) != (1, 0) or mode == 3 and K % 4:
                         continue
                     c = api.Config(W=cfg.W, F=max(1, min(cfg.F, 2)), V=V, S=S, G=cfg.G,
                                    mode=mode, sg_override=0)
-                    if mode in (3, 4):
+                    if mode == 3:
                         c.F, c.G = 2, 4 if K == 32 else 8
                     A.run(B, C, c)
                 # fan-out: two peer copies of C

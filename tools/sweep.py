@@ -104,7 +104,7 @@ def sweep_graph(g, Ks, iters, flush, stream, Ws, VS=((1, 0), (1, 1), (2, 0), (2,
             if 2 in modes and K % 32 == 0:  # TMA gather engine: only W matters
                 points += [(2, W, 0, 0, 0) for W in (1, 2, 4, 8)
                            if W * 8 * 16 * min(K, 256) <= 227 * 1024]
-            for m in (3, 4):  # short-row engines
+            for m in (3,):  # short-row engine
                 if m in modes and V == 1 and S == 0 and K % 4 == 0:
                     for F in (1, 2, 4):
                         G = 1
@@ -160,7 +160,7 @@ def recheck_graph(g, recs, top, iters, flush, stream):
         d = api.pspmm_decide_config(api.pspmm_features_compute(g.n, g.nnz, rp, ci), K).as_dict()
         key = lambda t: (t["V"], t["S"], t["W"], t["F"], t["G"], t.get("mode", 0),
                          t.get("order", 0))
-        if d["mode"] in (0, 2, 3, 4) and key(d) not in {key(t) for t in cands}:
+        if d["mode"] in (0, 2, 3) and key(d) not in {key(t) for t in cands}:
             cands.append({k: d[k] for k in ("V", "S", "W", "F", "G", "mode", "order")})
         B = torch.rand((g.n, K), device="cuda") * 2 - 1
         C = torch.empty((g.n, K), device="cuda")

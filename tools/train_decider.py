@@ -101,7 +101,7 @@ def guard_label(r, lab):
     mode, V, S, W, F, P, order = lab
     f = r["features"]
     K = r["K"]
-    if mode in (3, 4) and (K % 4 != 0 or f["d_max"] > 64.0):
+    if mode == 3 and (K % 4 != 0 or f["d_max"] > 64.0):
         mode = 0
     if V == 2 and f["pr2"] >= 0.45:
         V = 1
