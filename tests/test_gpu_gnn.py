@@ -65,6 +65,35 @@ def test_dense_gemm_tensor_core_shapes(n, Ki, Ko, pad, force_cc, monkeypatch):
         assert np.isnan(T[:, Ko:]).all(), "padding columns of T were written"
 
 
+@pytest.mark.parametrize("env", [{}, {"PSPMM_GEMM_OB": "1"}, {"PSPMM_GEMM_OB": "0"},
+                                 {"PSPMM_GEMM_WT": "0"}, {"PSPMM_GEMM_WT128": "1"}])
+@pytest.mark.parametrize("n,Ki,Ko,pad", [(1, 32, 128, 0), (127, 96, 128, 4), (5000, 64, 128, 0),
+                                         (300, 128, 128, 8), (2049, 64, 256, 0),
+                                         (1000, 128, 256, 4)])
+def test_dense_gemm_w_in_tmem(n, Ki, Ko, pad, env, monkeypatch):
+    """The W-in-TMEM form (Ko == 128, Ki <= 128: T^T = W^T X^T with W^T as
+    the tensor-memory A operand), with two / one / no staged output tiles,
+    against the shared-memory form (PSPMM_GEMM_WT=0) and as 128-column blocks
+    of Ko = 256 (PSPMM_GEMM_WT128=1); ragged tiles and padded ld."""
+    import torch
+    from paper_2605_15695_b200 import api
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    X = gen.dense(n, Ki, 41)
+    W = gen.dense(Ki, Ko, 42)
+    Xb = torch.zeros((n, Ki + pad), device="cuda")
+    Xb[:, :Ki] = torch.from_numpy(X).cuda()
+    Tb = torch.full((n, Ko + pad), float("nan"), device="cuda")
+    api.pspmm_dense_gemm(Xb[:, :Ki], torch.from_numpy(W).cuda(), Tb[:, :Ko])
+    torch.cuda.synchronize()
+    ref = X.astype(np.float64) @ W.astype(np.float64)
+    mag = np.abs(X.astype(np.float64)) @ np.abs(W.astype(np.float64))
+    T = Tb.cpu().numpy()
+    _check(T[:, :Ko], ref, mag, f"gemm {n}x{Ki}x{Ko} pad {pad} {env}")
+    if pad:
+        assert np.isnan(T[:, Ko:]).all(), "padding columns of T were written"
+
+
 @pytest.mark.parametrize("name", ["reddit_s", "roadnet_s", "empty_rows"])
 @pytest.mark.parametrize("Ki,Ko", [(64, 32), (32, 64), (48, 48), (128, 16), (64, 64),
                                    (128, 128)])
