@@ -393,10 +393,14 @@ def measure_single(g, steps, warmup, flush, stream, want_cusparse=True, want_e2e
         tl = time_steps(lambda: api.pspmm_gnn_layer(A, Bd, Wd, T, Y, cfg, stream), 5, 2, flush,
                         stream)
         tg = time_steps(lambda: api.pspmm_dense_gemm(Bd, Wd, T, stream), 5, 2, flush, stream)
-        ml, mg = float(np.mean(tl)), float(np.mean(tg))
+        # the same bytes moved by a plain device copy: the practical ceiling
+        # of a ~100 MB transfer (launch, ramp and drain included)
+        tc = time_steps(lambda: T.copy_(Bd), 5, 2, flush, stream)
+        ml, mg, mc = float(np.mean(tl)), float(np.mean(tg)), float(np.mean(tc))
         lf = 2.0 * g.nnz * K + 2.0 * g.n * K * K
         out["gnn_layer"] = {"ms": ml, "gflops": lf / (ml * 1e-3) / 1e9, "dense_gemm_ms": mg,
                             "dense_gemm_gbs": 8.0 * g.n * K / (mg * 1e-3) / 1e9,
+                            "device_copy_ms": mc, "dense_gemm_over_copy": mc / mg,
                             "what": f"pspmm_gnn_layer: Y = A (X W), W {K}x{K}; flops 2 nnz K + "
                                     "2 n K^2; dense_gemm_gbs = X read + T written"}
     del A, A_dec, rp, ci, vl, Bd, C

@@ -28,10 +28,14 @@
 //  - warps 5-8 (epilogue): tcgen05.ld 32x32b (warp w reads TMEM lanes
 //    32 (w % 4) .. + 31 = rows of the tile), the tile written into a
 //    128-B-swizzled shared buffer and stored by one thread with TMA tensor
-//    stores (two buffers: a store drains while the next tile is staged), so
-//    the next tile's MMAs overlap this epilogue.
+//    stores (one buffer by default: the next tile is staged once the store
+//    has read it; two on request), and the next tile's MMAs overlap this
+//    epilogue.
 // W's rna hi / lo image (all of Ki x Ko, or a column block of it) is built
-// once per CTA in shared memory.  The dropped terms (lo's own truncation,
+// once per CTA in shared memory.  For Ko == 128 (and 128-column blocks of
+// wider W) with Ki <= 128, gemm_tc_wt_kernel computes T^T = W^T . X^T with
+// W^T as the A operand in tensor memory instead, which frees shared memory
+// for the rings.  The dropped terms (lo's own truncation,
 // lo.lo) are < 2^-20 relative per product, inside the c-1 bound.
 // History and measurements: DESIGN.md section 5 (a plain device copy of the
 // same bytes is the practical ceiling at these sizes).
@@ -417,6 +421,258 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// kind::tf32 instruction descriptor for an M x N tile (D fp32, A / B TF32,
+// both K-major)
+__device__ __forceinline__ uint32_t idesc_mn(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+// D[tmem] (+)= A[tmem] . B[smem]: the A operand read from tensor memory
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a, uint64_t db, uint32_t id,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+// The W-in-TMEM form, for Ko == 128 and Ki <= 128: the product is computed
+// transposed, T^T = W^T . X^T, so W^T (M = Ko = 128 rows, K = Ki) is the A
+// operand and lives in tensor memory (its hi and lo images: 2 Ki of the 512
+// columns; the epilogue warps write them once per CTA with tcgen05.st), X^T
+// is the B operand (N = 128 tile rows, K-major: the TMA chunk exactly as in
+// gemm_tc_ring_kernel, and its lo), and D^T (lane = output column, column =
+// tile row) is double-buffered in the other 256 columns.  Shared memory then
+// holds only the X / lo rings and the staged output tiles: W's 128-KB image
+// no longer crowds them out.  Epilogue: warp q owns output columns
+// 32q .. 32q + 31 (TMEM lanes), i.e. exactly one 32-column block of the
+// TMA store; a thread writes its column of 128 rows into the 128-B-swizzled
+// tile (one conflict-free 128-B row per warp store).
+constexpr int kWtD = 0, kWtW = 256;  // TMEM columns: D buffers at 0 / 128, W^T at 256
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_wt_kernel(const __grid_constant__ CUtensorMap xmap,
+                      const __grid_constant__ CUtensorMap tmap, const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int Ki = a.Ki, SX = a.x_stages, SL = a.lo_stages, OB = a.out_bufs;
+  constexpr int Ko = 128;
+  uint8_t *xst0 = smem;                              // SX x 16 KB X chunks
+  uint8_t *lost0 = xst0 + (size_t)SX * kChunkPart;   // SL x 16 KB lo chunks
+  uint8_t *otile = lost0 + (size_t)SL * kChunkPart;  // OB x [4 blocks of 128 rows x 128 B]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(otile + (size_t)OB * kM * Ko * 4);
+  uint64_t *xfull = bar, *xempty = bar + SX, *lofull = bar + 2 * SX, *loempty = lofull + SL;
+  uint64_t *accf = loempty + SL, *acce = accf + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acce + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tiles = (a.n + kM - 1) / kM;
+  const int chunks = Ki / kKc;
+
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < SX; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);
+    }
+    for (int s = 0; s < SL; ++s) {
+      mbar_init(&lofull[s], kLoaders);
+      mbar_init(&loempty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], kEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();  // barriers initialised, TMEM address published
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 9) {  // TMA producer: starts at once
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x)
+        for (int c = 0; c < chunks; ++c, ++it) {
+          const int s = it % SX;
+          if (it >= SX) mbar_wait(&xempty[s], ((it / SX) - 1) & 1);
+          mbar_expect_tx(&xfull[s], kChunkPart);
+          tma_2d(smem_u32(xst0 + (size_t)s * kChunkPart), &xmap, &xfull[s], c * kKc,
+                 (int)(t * kM));
+        }
+    }
+    __syncwarp();
+  } else if (warp < 4) {  // splitters (as gemm_tc_ring_kernel)
+    int it = 0;
+    const uint32_t sw = (uint32_t)(tid & 7);
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int c = 0; c < chunks; ++c, ++it) {
+        const int sx = it % SX, sl = it % SL;
+        mbar_wait(&xfull[sx], (it / SX) & 1);
+        if (it >= SL) mbar_wait(&loempty[sl], ((it / SL) - 1) & 1);
+        const uint32_t xr = smem_u32(xst0 + (size_t)sx * kChunkPart) + tid * 128;
+        const uint32_t lr = smem_u32(lost0 + (size_t)sl * kChunkPart) + tid * 128;
+        uint4 x[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x[g].x), "=r"(x[g].y), "=r"(x[g].z), "=r"(x[g].w)
+                       : "r"(xr + ((g ^ sw) << 4)));
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const float4 lo = make_float4(
+              __uint_as_float(x[g].x) - __uint_as_float(x[g].x & 0xFFFFE000u),
+              __uint_as_float(x[g].y) - __uint_as_float(x[g].y & 0xFFFFE000u),
+              __uint_as_float(x[g].z) - __uint_as_float(x[g].z & 0xFFFFE000u),
+              __uint_as_float(x[g].w) - __uint_as_float(x[g].w & 0xFFFFE000u));
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lr + ((g ^ sw) << 4)),
+                       "f"(lo.x), "f"(lo.y), "f"(lo.z), "f"(lo.w)
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&lofull[sl]);
+      }
+    }
+  } else if (warp == 4) {  // MMA issuer: waits for W^T in TMEM (named barrier 2)
+    asm volatile("bar.sync 2, %0;" ::"r"(32 + kEpi) : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (lane == 0) {
+      const uint32_t id = idesc_mn(Ko, kM);
+      const uint32_t whi = tmem + kWtW, wlo = whi + (uint32_t)Ki;
+      int it = 0, tl = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        const int b = tl & 1;
+        if (tl >= 2) mbar_wait(&acce[b], ((tl >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + kWtD + (uint32_t)(b * kM);
+        for (int c = 0; c < chunks; ++c, ++it) {
+          const int sx = it % SX, sl = it % SL;
+          mbar_wait(&lofull[sl], (it / SL) & 1);  // the splitters saw xfull: X landed too
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t xhi = smem_u32(xst0 + (size_t)sx * kChunkPart);
+          const uint32_t xlo = smem_u32(lost0 + (size_t)sl * kChunkPart);
+#pragma unroll
+          for (int ks = 0; ks < kKc / 8; ++ks) {
+            const uint64_t dbh = desc_sw128(xhi + ks * 32), dbl = desc_sw128(xlo + ks * 32);
+            const uint32_t k0 = (uint32_t)(c * kKc + ks * 8);  // TMEM column of this K step
+            mma_tf32_ts(acc, whi + k0, dbh, id, (c > 0 || ks > 0) ? 1u : 0u);
+            mma_tf32_ts(acc, wlo + k0, dbh, id, 1u);
+            mma_tf32_ts(acc, whi + k0, dbl, id, 1u);
+          }
+          mma_commit(&xempty[sx]);
+          mma_commit(&loempty[sl]);
+        }
+        mma_commit(&accf[b]);
+      }
+    }
+    __syncwarp();
+  } else {  // warps 5-8: W^T -> TMEM once, then the epilogue
+    const int q = warp & 3;  // TMEM lane quarter = output columns 32q .. 32q + 31
+    const int col = 32 * q + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+    for (int k0 = 0; k0 < Ki; k0 += 16) {  // W[k][col] for 16 k: coalesced over the warp
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float w = __ldg(a.W + (int64_t)(k0 + j) * a.ldw + col);
+        const float h = tf32_rn(w);
+        hi[j] = __float_as_uint(h);
+        lo[j] = __float_as_uint(tf32_rn(w - h));
+      }
+      tmem_st16(lane_base + kWtW + k0, hi);
+      tmem_st16(lane_base + kWtW + Ki + k0, lo);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync 2, %0;" ::"r"(32 + kEpi) : "memory");
+    const bool leader = tid == kLoaders + 32;
+    int tl = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+      const int b = tl & 1;
+      mbar_wait(&accf[b], (tl >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tb = lane_base + kWtD + (uint32_t)(b * kM);  // columns = tile rows
+      if (OB > 0) {
+        uint8_t *ot = otile + (size_t)(OB == 2 ? (tl & 1) : 0) * kM * Ko * 4 +
+                      (size_t)q * kM * 128;  // this warp's 32-column block
+        if (leader) {
+          if (OB == 2)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+        const uint32_t obase = smem_u32(ot) + (uint32_t)(lane & 3) * 4;
+        for (int r0 = 0; r0 < kM; r0 += 64) {
+          uint32_t v[4][16];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) tmem_ld16_nowait(tb + r0 + 16 * u, v[u]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int r = r0 + 16 * u + j;  // tile row; chunk (lane / 4) of row r, swizzled
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(obase + r * 128 +
+                                                          ((((uint32_t)lane >> 2) ^ (r & 7)) << 4)),
+                           "r"(v[u][j])
+                           : "memory");
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&acce[b]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+        if (leader) {
+          uint8_t *ob = otile + (size_t)(OB == 2 ? (tl & 1) : 0) * kM * Ko * 4;
+          for (int blk = 0; blk < Ko / 32; ++blk)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmap)),
+                "r"(blk * 32), "r"((int)(t * kM)), "r"(smem_u32(ob + (size_t)blk * kM * 128))
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        continue;
+      }
+      // no staged tile: each thread stores its column, 32 consecutive
+      // columns per warp store (128 B per row)
+      for (int r0 = 0; r0 < kM; r0 += 16) {
+        float v[16];
+        tmem_ld16(tb + r0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int64_t row = t * kM + r0 + j;
+          if (row < a.n) __stcs(a.T + row * a.ldt + col, v[j]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acce[b]);
+    }
+    if (OB > 0 && leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 int tmem_cols_for(int Ko) {
   int c = 32;
   while (c < 2 * Ko) c <<= 1;
@@ -459,7 +715,14 @@ pspmm_status gemm_tc_one(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, in
 pspmm_status gemm_tc(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, int64_t ldx,
                      const float *d_W, int64_t ldw, float *d_T, int64_t ldt, cudaStream_t stream) {
   if (n == 0) return PSPMM_OK;
-  const int b = gemm_tc_block(Ki, Ko);
+  int b = gemm_tc_block(Ki, Ko);
+  // Ko a multiple of 128 and Ki <= 128: 128-column blocks on the W-in-TMEM
+  // form (64 x 256: 82.5 us for two blocks vs 112.6 us for one shared-memory
+  // launch); PSPMM_GEMM_WT=0 / PSPMM_GEMM_WT128=0 (A/B
+  // knobs) keep the widest shared-memory block
+  const char *wte = std::getenv("PSPMM_GEMM_WT"), *w128 = std::getenv("PSPMM_GEMM_WT128");
+  if (Ko % 128 == 0 && Ki <= 128 && !(wte && wte[0] == '0') && !(w128 && w128[0] == '0'))
+    b = 128;
   if (b <= 0) PSPMM_FAIL(PSPMM_ERR_UNSUPPORTED, "dense_gemm: no tensor-core column block fits");
   for (int j0 = 0; j0 < Ko; j0 += b) {  // T[:, j0:j0+b] = X . W[:, j0:j0+b]
     pspmm_status st = gemm_tc_one(n, Ki, std::min(b, Ko - j0), d_X, ldx, d_W + j0, ldw, d_T + j0,
@@ -488,15 +751,19 @@ pspmm_status gemm_tc_one(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, in
     PSPMM_FAIL(PSPMM_ERR_CUDA, "dense_gemm: tensor map encode failed");
   // ring depths: 2 lo buffers (PSPMM_GEMM_LO, 2..4), as many X stages as fit
   // (<= 8, PSPMM_GEMM_XS caps it), and the most staged output buffers
-  // (PSPMM_GEMM_OB caps it; Ko % 32 == 0) that leave >= 4 X stages for two
+  // (PSPMM_GEMM_OB sets it; Ko % 32 == 0) that leave >= 4 X stages for two
   // buffers, >= 3 for one; without a staged epilogue >= 2.  The knobs are
   // A/B switches for tools/gemm_forms.py.
   int sl = 2;
   if (const char *e = std::getenv("PSPMM_GEMM_LO")) sl = std::max(2, std::min(4, std::atoi(e)));
   int xcap = 8;
   if (const char *e = std::getenv("PSPMM_GEMM_XS")) xcap = std::max(2, std::min(8, std::atoi(e)));
-  int obmax = Ko % 32 == 0 ? 2 : 0;
-  if (const char *e = std::getenv("PSPMM_GEMM_OB")) obmax = std::max(0, std::min(obmax, std::atoi(e)));
+  // one staged output tile by default: the X stages it leaves pay more than
+  // a second tile (W-in-TMEM 128 x 128: 53.5 us vs 61.4 us with two tiles
+  // and 4 stages; shared-memory form 128 x 64: 53.2 vs 55.3 us)
+  int obmax = Ko % 32 == 0 ? 1 : 0;
+  if (const char *e = std::getenv("PSPMM_GEMM_OB"))
+    obmax = Ko % 32 == 0 ? std::max(0, std::min(2, std::atoi(e))) : 0;
   CUtensorMap tmapT;
   std::memset(&tmapT, 0, sizeof(tmapT));
   if (obmax > 0) {
@@ -507,6 +774,43 @@ pspmm_status gemm_tc_one(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, in
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       obmax = 0;
+  }
+  const int64_t tiles = (n + kM - 1) / kM;
+  const int grid = (int)std::min<int64_t>(tiles, num_sms());
+  // Ko == 128, Ki <= 128: W^T in tensor memory (gemm_tc_wt_kernel), no W
+  // image in shared memory; PSPMM_GEMM_WT=0 (A/B knob) keeps the ring form
+  const char *wte = std::getenv("PSPMM_GEMM_WT");
+  if (Ko == 128 && Ki <= 128 && !(wte && wte[0] == '0')) {
+    int ob = -1, sx = 0;
+    for (int o = obmax; o >= 0; --o) {
+      const int64_t left = kMaxSmem - kSmemSlack - (int64_t)o * otile - (int64_t)sl * kChunkPart;
+      const int s = (int)std::min<int64_t>(xcap, left / kChunkPart);
+      if (s >= (o == 2 ? 4 : o == 1 ? 3 : 2)) {
+        ob = o;
+        sx = s;
+        break;
+      }
+    }
+    GemmArgs args;
+    args.X = d_X;
+    args.W = d_W;
+    args.T = d_T;
+    args.n = n;
+    args.ldx = ldx;
+    args.ldw = ldw;
+    args.ldt = ldt;
+    args.Ki = Ki;
+    args.Ko = Ko;
+    args.x_stages = sx;
+    args.lo_stages = sl;
+    args.out_bufs = ob;
+    args.tmem_cols = 512;
+    const size_t smem = (size_t)(kSmemSlack + (int64_t)ob * otile + (int64_t)(sx + sl) * kChunkPart);
+    PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_wt_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gemm_tc_wt_kernel<<<grid, kThreads, smem, stream>>>(map, tmapT, args);
+    PSPMM_CUDA_TRY(cudaGetLastError());
+    return PSPMM_OK;
   }
   int ob = -1, sx = 0;
   for (int o = obmax; o >= 0; --o) {
@@ -533,8 +837,6 @@ pspmm_status gemm_tc_one(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, in
   args.lo_stages = sl;
   args.out_bufs = ob;
   args.tmem_cols = tmem_cols_for(Ko);
-  const int64_t tiles = (n + kM - 1) / kM;
-  const int grid = (int)std::min<int64_t>(tiles, num_sms());
   const size_t smem = (size_t)(kSmemSlack + w + (int64_t)ob * otile + (int64_t)(sx + sl) * kChunkPart);
   PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_ring_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

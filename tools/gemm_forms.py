@@ -17,13 +17,16 @@ sys.path.insert(0, ROOT)
 # (the round-2 A/B of the earlier "direct" form, one 32-KB stage per X chunk
 # holding X and its lo, against these: profiles/r02/gemm_r3/gemm_forms.jsonl)
 VARIANTS = [
-    ("ring", {}),
+    ("default", {}),
+    ("ring", {"PSPMM_GEMM_WT": "0"}),
+    ("no_wt128", {"PSPMM_GEMM_WT128": "0"}),
+    ("ob2", {"PSPMM_GEMM_OB": "2"}),
     ("ring_lo3", {"PSPMM_GEMM_LO": "3"}),
     ("ring_xs4", {"PSPMM_GEMM_XS": "4"}),
     ("ring_ob1", {"PSPMM_GEMM_OB": "1"}),
     ("ring_ob0", {"PSPMM_GEMM_OB": "0"}),
 ]
-KNOBS = ("PSPMM_GEMM_LO", "PSPMM_GEMM_XS", "PSPMM_GEMM_OB")
+KNOBS = ("PSPMM_GEMM_LO", "PSPMM_GEMM_XS", "PSPMM_GEMM_OB", "PSPMM_GEMM_WT", "PSPMM_GEMM_WT128")
 
 
 def main():
