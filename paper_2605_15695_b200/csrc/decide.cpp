@@ -20,6 +20,9 @@ namespace {
 // B200 L2 (cudaDevAttrL2CacheSize on the target; the decider is a pure host
 // function of (features, K), so the target's value is a constant here)
 constexpr double kL2Bytes = 132644864.0;
+// resident mode-0 warps: 148 SMs x 24 warps (the engine's launch bounds,
+// 256 threads x 3 blocks per SM)
+constexpr double kSMs = 148.0, kWarpsPerSM = 24.0;
 
 int ceil_pow2(int x) {
   int p = 1;
@@ -130,6 +133,19 @@ extern "C" pspmm_status pspmm_decide_config(const pspmm_features *f, int32_t K,
         c.F = (q + 31) / 32;
         c.G = ceil_pow2((q + c.F - 1) / c.F);
       }
+    }
+    // sub-wave hub rows: when every S = 0 unit fits in one wave of resident
+    // row groups (148 SMs x 24 warps x 32 / G), the launch lasts as long as
+    // its longest row, so rows of >= 4 SG nonzeros (Eq. 3) are split (S = 1,
+    // P:130).  On the training corpus this regime holds 18 (graph, K) points;
+    // S = 1 is the sweep's best on all 18 and the forest already picks it on
+    // all 18 (the guard changes no corpus decision); it covers graphs outside
+    // the corpus such as Cora (d_max = 4.5-5 SG: K = 32 S = 0 20.5 us vs
+    // S = 1 13.3 us)
+    if (c.mode == 0 && c.V == 1 && c.S == 0 && c.G >= 1) {
+      const double sg = std::ceil(f->d_hat / 32.0) * 32.0;
+      const double groups = kSMs * kWarpsPerSM * (32.0 / c.G);
+      if (f->n <= groups && f->d_max >= 4.0 * sg) c.S = 1;
     }
     *out = c;
     return PSPMM_OK;

@@ -85,6 +85,9 @@ def test_c_decider_evaluates_the_header_tree():
             # the single-pass guard for B far beyond L2 (decide.cpp)
             F = -(-q // 32)
             G = ceil_pow2(-(-q // F))
+        if (mode == 0 and V == 1 and S == 0 and
+                n <= 148 * 24 * (32 / G) and f["d_max"] >= 4 * (-(-f["d_hat"] // 32) * 32)):
+            S = 1  # the sub-wave hub guard (decide.cpp)
         if mode == 2 and K % 32 == 0:
             assert (c.mode, c.V, c.S, c.W) == (2, V, S, W)
         elif mode == 3 and K % 4 == 0:
@@ -133,3 +136,17 @@ def test_trainer_recovers_planted_rule():
     root = td.fit(X, perf, 4, 3)
     ev = td.evaluate(recs, keys, X, perf, list(range(len(recs))), root)
     assert ev["pre"] > 0.99 and ev["rnd"] < 0.8
+
+
+def test_sub_wave_hub_guard():
+    """Every S = 0 unit in one wave and rows of >= 4 SG nonzeros: split them
+    (S = 1), at every K; Cora-shaped features (n = 2708, d_max = 168, SG =
+    32).  (Graphs outside the regime: test_c_decider_evaluates_the_header_tree
+    mirrors the guard over 400 random feature vectors.)"""
+    from paper_2605_15695_b200 import api
+    cora = dict(n=2708.0, n_hat=2485.0, nnz=10556.0, delta=0.918, d=3.9, d_hat=4.25,
+                d_max=168.0, cv=1.56, cv_hat=1.47, sr1=1.01, sr2=1.02, rho=0.00144, b=1078.0,
+                b_max=2706.0, pr1=0.0, pr2=0.5)
+    for K in (16, 32, 64, 128, 256):
+        c = api.pspmm_decide_config(cora, K)
+        assert c.mode != 0 or c.V != 1 or c.S == 1, (K, c)

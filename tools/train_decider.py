@@ -107,6 +107,13 @@ def guard_label(r, lab):
         V = 1
     if mode == 0 and P > 1 and f["n"] * K * 4.0 > 2.0 * L2_BYTES and (((K + 3) // 4) + 31) // 32 <= 8:
         F, P = ((K + 3) // 4 + 31) // 32, 1
+    if mode == 0 and V == 1 and S == 0:  # the sub-wave hub guard
+        q = (K + 3) // 4
+        G = 1
+        while G < -(-q // (F * P)) and G < 32:
+            G <<= 1
+        if f["n"] <= 148 * 24 * (32 / G) and f["d_max"] >= 4 * (-(-f["d_hat"] // 32) * 32):
+            S = 1
     return (mode, V, S, W, F, P, order if mode == 0 else 0)
 
 
