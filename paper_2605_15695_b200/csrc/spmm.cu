@@ -15,21 +15,29 @@ using namespace detail;
 // bound copy at once).
 __global__ void zero_split_kernel(const int32_t *__restrict__ split, int64_t num_split, int V,
                                   int64_t n_rows, int32_t K, float *__restrict__ C, int64_t ldc,
-                                  int mc) {
+                                  int mc, int vec4) {
   // the engine (a programmatic dependent) may launch now; it waits for this
   // grid's completion before its first write
   asm volatile("griddepcontrol.launch_dependents;");
-  const int64_t per = (int64_t)V * K;
+  const int64_t q = vec4 ? K / 4 : K;  // stores per row
+  const int64_t per = (int64_t)V * q;
   const int64_t total = num_split * per;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = t / per, r = t % per;
-    const int64_t row = (int64_t)split[s] * V + r / K;
-    if (row < n_rows) {
-      if (mc)
-        mc_st(C + row * ldc + r % K, 0.f);
-      else
-        C[row * ldc + r % K] = 0.f;
+    const int64_t s = t / per, r = t - s * per;
+    const int64_t k = r / q, j = r - k * q;
+    const int64_t row = (int64_t)split[s] * V + k;
+    if (row >= n_rows) continue;
+    float *p = C + row * ldc + (vec4 ? 4 * j : j);
+    if (vec4 && !mc) {
+      *reinterpret_cast<float4 *>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      for (int e = 0; e < (vec4 ? 4 : 1); ++e) {
+        if (mc)
+          mc_st(p + e, 0.f);
+        else
+          p[e] = 0.f;
+      }
     }
   }
 }
@@ -149,10 +157,12 @@ pspmm_status prepare_c(const pspmm_pcsr_s *A, int32_t K, float *d_C, int64_t ldc
                                                                     fan.mc);
       PSPMM_CUDA_TRY(cudaGetLastError());
     } else if (A->S == 1 && A->num_split > 0) {
-      const int64_t total = A->num_split * A->V * (int64_t)K;
+      // float4 stores when every row start is 16-B aligned
+      const int vec4 = K % 4 == 0 && ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+      const int64_t total = A->num_split * A->V * (int64_t)(vec4 ? K / 4 : K);
       const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
       zero_split_kernel<<<blocks, 256, 0, stream>>>(A->d_split, A->num_split, A->V, A->n_rows,
-                                                     K, C, ldc, fan.mc);
+                                                     K, C, ldc, fan.mc, vec4);
       PSPMM_CUDA_TRY(cudaGetLastError());
     }
   }

@@ -278,10 +278,6 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
   constexpr int U1 = U0 < TILE ? U0 : TILE;
   constexpr int U = U1 >= 16 ? 16 : U1 >= 8 ? 8 : U1 >= 4 ? 4 : U1 >= 2 ? 2 : 1;
   static_assert(TILE % U == 0, "tile/batch mismatch");
-  // S = 1 launched as a programmatic dependent of the split-row zeroing
-  // kernel (PDL): this grid starts while the zeroing runs and waits for it
-  // here, before any of its writes (a no-op without the launch attribute)
-  if (S == 1) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int lane = threadIdx.x & 31;
   const int g = lane / G;
@@ -357,6 +353,11 @@ __global__ void __launch_bounds__(PSPMM_MAX_THREADS, PSPMM_MIN_BLOCKS)
       }
     }
   } else {
+    // S = 1 is launched as a programmatic dependent of the split-row zeroing
+    // kernel (PDL): the grid starts while the zeroing runs, gathers its first
+    // unit, and waits for the zeroing only here, before its first write (a
+    // no-op without the launch attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int panel = a.trow[unit];
     const bool sole = (unit == 0 || a.trow[unit - 1] != panel) &&
                       (unit + 1 == a.units_total || a.trow[unit + 1] != panel);
