@@ -17,6 +17,31 @@ import numpy as np
 from . import api
 
 
+class _nvtx:
+    """NVTX range around a multi-GPU step phase (exchange / SpMM), so an
+    Nsight Systems timeline shows how the collective overlaps the engine
+    (SURVEY §5); a no-op where NVTX is unavailable."""
+
+    def __init__(self, name):
+        self.name = name
+        self.on = False
+
+    def __enter__(self):
+        try:
+            import torch
+            torch.cuda.nvtx.range_push(self.name)
+            self.on = True
+        except Exception:
+            pass
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            import torch
+            torch.cuda.nvtx.range_pop()
+        return False
+
+
 @dataclass
 class Shard:
     rank: int
@@ -133,8 +158,10 @@ class ShardedSpmm:
     def step(self, B_padded, stream=None, group=None):
         """All-gather the padded B shards, then the local SpMM.  Returns the
         padded local C (the next layer's B shard)."""
-        all_gather_rows(B_padded, self.B_full, group)
-        self.A.run(self.B_full, self.C, self.cfg, stream)
+        with _nvtx("pspmm allgather"):
+            all_gather_rows(B_padded, self.B_full, group)
+        with _nvtx("pspmm spmm"):
+            self.A.run(self.B_full, self.C, self.cfg, stream)
         return self.C
 
     def step_overlap(self, B_padded, stream=None, group=None):
@@ -143,11 +170,14 @@ class ShardedSpmm:
         import torch.distributed as dist
         if self.A_own is None or dist.get_backend(group) != "nccl":
             return self.step(B_padded, stream, group)
-        work = dist.all_gather_into_tensor(self.B_full, B_padded, group=group, async_op=True)
-        self.A_own.run(B_padded, self.C, self.cfg, stream)
-        work.wait()  # the compute stream waits for the gathered rows
+        with _nvtx("pspmm allgather || own-column spmm"):
+            work = dist.all_gather_into_tensor(self.B_full, B_padded, group=group,
+                                               async_op=True)
+            self.A_own.run(B_padded, self.C, self.cfg, stream)
+            work.wait()  # the compute stream waits for the gathered rows
         if self.A_rem is not None:
-            api.pspmm_spmm_accumulate(self.A_rem, self.B_full, self.C, self.cfg, stream)
+            with _nvtx("pspmm remote-column spmm"):
+                api.pspmm_spmm_accumulate(self.A_rem, self.B_full, self.C, self.cfg, stream)
         return self.C
 
 
@@ -236,12 +266,14 @@ class FanoutSpmm:
         benchmarking).  Returns this rank's output rows."""
         src, dst = self.cur, 1 - self.cur
         out = self.own(dst)
-        api.pspmm_spmm_run_fanout(self.A, self.X[src], out, self.peers[dst], self.cfg, stream,
-                                  K=self.K)
+        with _nvtx("pspmm spmm + fan-out stores"):
+            api.pspmm_spmm_run_fanout(self.A, self.X[src], out, self.peers[dst], self.cfg,
+                                      stream, K=self.K)
         if swap:
             self.cur = dst
         if barrier:
-            self.barrier(group)
+            with _nvtx("pspmm layer barrier"):
+                self.barrier(group)
         return out
 
     def close(self):
@@ -292,11 +324,14 @@ class MulticastSpmm(FanoutSpmm):
     def step(self, stream=None, group=None, swap=True, barrier=True):
         src, dst = self.cur, 1 - self.cur
         out = self.own(dst)
-        api.pspmm_spmm_run_multicast(self.A, self.X[src], out, self._mc[dst], self.cfg, stream)
+        with _nvtx("pspmm spmm + multimem stores"):
+            api.pspmm_spmm_run_multicast(self.A, self.X[src], out, self._mc[dst], self.cfg,
+                                         stream)
         if swap:
             self.cur = dst
         if barrier:
-            self.barrier(group)
+            with _nvtx("pspmm layer barrier"):
+                self.barrier(group)
         return out
 
     def close(self):
@@ -483,6 +518,8 @@ class HaloSpmm:
 
     def step(self, stream=None, group=None):
         """B_local must hold this layer's input rows; returns C (rows x K)."""
-        self.exchange(group, stream)
-        self.A.run(self.B_ext, self.C, self.cfg, stream)
+        with _nvtx("pspmm halo exchange"):
+            self.exchange(group, stream)
+        with _nvtx("pspmm spmm"):
+            self.A.run(self.B_ext, self.C, self.cfg, stream)
         return self.C
