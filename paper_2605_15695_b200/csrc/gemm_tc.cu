@@ -164,6 +164,59 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap *map, uin
       : "memory");
 }
 
+// The TMA producer of both kernels: X chunk (tile t, chunk c) into X stage
+// it % SX once the MMA has released the stage's previous use.
+__device__ __forceinline__ void tma_x_loop(const CUtensorMap *xmap, int64_t tiles, int chunks,
+                                           int SX, uint8_t *xst0, uint64_t *xfull,
+                                           uint64_t *xempty) {
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x)
+    for (int c = 0; c < chunks; ++c, ++it) {
+      const int s = it % SX;
+      if (it >= SX) mbar_wait(&xempty[s], ((it / SX) - 1) & 1);
+      mbar_expect_tx(&xfull[s], kChunkPart);
+      tma_2d(smem_u32(xst0 + (size_t)s * kChunkPart), xmap, &xfull[s], c * kKc, (int)(t * kM));
+    }
+}
+
+// The splitters of both kernels (warps 0-3, thread = row of the chunk): for
+// every X chunk, lo = x - trunc(x) (exact in fp32) into lo buffer it % SL,
+// in the chunk's own 128-B swizzle, then a proxy fence and an arrive.
+__device__ __forceinline__ void split_loop(int tid, int64_t tiles, int chunks, int SX, int SL,
+                                           const uint8_t *xst0, uint8_t *lost0, uint64_t *xfull,
+                                           uint64_t *lofull, uint64_t *loempty) {
+  int it = 0;
+  const uint32_t sw = (uint32_t)(tid & 7);
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int c = 0; c < chunks; ++c, ++it) {
+      const int sx = it % SX, sl = it % SL;
+      mbar_wait(&xfull[sx], (it / SX) & 1);
+      if (it >= SL) mbar_wait(&loempty[sl], ((it / SL) - 1) & 1);
+      const uint32_t xr = smem_u32(xst0 + (size_t)sx * kChunkPart) + tid * 128;
+      const uint32_t lr = smem_u32(lost0 + (size_t)sl * kChunkPart) + tid * 128;
+      uint4 x[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(x[g].x), "=r"(x[g].y), "=r"(x[g].z), "=r"(x[g].w)
+                     : "r"(xr + ((g ^ sw) << 4)));
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const float4 lo = make_float4(
+            __uint_as_float(x[g].x) - __uint_as_float(x[g].x & 0xFFFFE000u),
+            __uint_as_float(x[g].y) - __uint_as_float(x[g].y & 0xFFFFE000u),
+            __uint_as_float(x[g].z) - __uint_as_float(x[g].z & 0xFFFFE000u),
+            __uint_as_float(x[g].w) - __uint_as_float(x[g].w & 0xFFFFE000u));
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lr + ((g ^ sw) << 4)),
+                     "f"(lo.x), "f"(lo.y), "f"(lo.z), "f"(lo.w)
+                     : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&lofull[sl]);
+    }
+  }
+}
+
 struct GemmArgs {
   const float *__restrict__ X;
   const float *__restrict__ W;
@@ -227,17 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();  // barriers initialised, TMEM address published
 
   if (warp == 9) {  // TMA producer: starts at once
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x)
-        for (int c = 0; c < chunks; ++c, ++it) {
-          const int s = it % SX;
-          if (it >= SX) mbar_wait(&xempty[s], ((it / SX) - 1) & 1);
-          mbar_expect_tx(&xfull[s], kChunkPart);
-          tma_2d(smem_u32(xst0 + (size_t)s * kChunkPart), &xmap, &xfull[s], c * kKc,
-                 (int)(t * kM));
-        }
-    }
+    if (lane == 0) tma_x_loop(&xmap, tiles, chunks, SX, xst0, xfull, xempty);
     __syncwarp();
   } else {
     {  // W -> hi / lo image (warps 0-8), then a barrier among those warps only
@@ -274,37 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     const uint32_t tmem = *tmem_slot;
-    if (warp < 4) {  // splitters: lo = x - trunc(x) into the lo ring, same swizzle
-      int it = 0;
-      const uint32_t sw = (uint32_t)(tid & 7);
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        for (int c = 0; c < chunks; ++c, ++it) {
-          const int sx = it % SX, sl = it % SL;
-          mbar_wait(&xfull[sx], (it / SX) & 1);
-          if (it >= SL) mbar_wait(&loempty[sl], ((it / SL) - 1) & 1);
-          const uint32_t xr = smem_u32(xst0 + (size_t)sx * kChunkPart) + tid * 128;
-          const uint32_t lr = smem_u32(lost0 + (size_t)sl * kChunkPart) + tid * 128;
-          uint4 x[8];
-#pragma unroll
-          for (int g = 0; g < 8; ++g)
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(x[g].x), "=r"(x[g].y), "=r"(x[g].z), "=r"(x[g].w)
-                         : "r"(xr + ((g ^ sw) << 4)));
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            const float4 lo = make_float4(
-                __uint_as_float(x[g].x) - __uint_as_float(x[g].x & 0xFFFFE000u),
-                __uint_as_float(x[g].y) - __uint_as_float(x[g].y & 0xFFFFE000u),
-                __uint_as_float(x[g].z) - __uint_as_float(x[g].z & 0xFFFFE000u),
-                __uint_as_float(x[g].w) - __uint_as_float(x[g].w & 0xFFFFE000u));
-            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lr + ((g ^ sw) << 4)),
-                         "f"(lo.x), "f"(lo.y), "f"(lo.z), "f"(lo.w)
-                         : "memory");
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&lofull[sl]);
-        }
-      }
+    if (warp < 4) {  // splitters
+      split_loop(tid, tiles, chunks, SX, SL, xst0, lost0, xfull, lofull, loempty);
     } else if (warp == 4) {  // MMA issuer
       if (lane == 0) {
         const uint32_t id = idesc(Ko);
@@ -504,49 +518,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 9) {  // TMA producer: starts at once
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x)
-        for (int c = 0; c < chunks; ++c, ++it) {
-          const int s = it % SX;
-          if (it >= SX) mbar_wait(&xempty[s], ((it / SX) - 1) & 1);
-          mbar_expect_tx(&xfull[s], kChunkPart);
-          tma_2d(smem_u32(xst0 + (size_t)s * kChunkPart), &xmap, &xfull[s], c * kKc,
-                 (int)(t * kM));
-        }
-    }
+    if (lane == 0) tma_x_loop(&xmap, tiles, chunks, SX, xst0, xfull, xempty);
     __syncwarp();
-  } else if (warp < 4) {  // splitters (as gemm_tc_ring_kernel)
-    int it = 0;
-    const uint32_t sw = (uint32_t)(tid & 7);
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-      for (int c = 0; c < chunks; ++c, ++it) {
-        const int sx = it % SX, sl = it % SL;
-        mbar_wait(&xfull[sx], (it / SX) & 1);
-        if (it >= SL) mbar_wait(&loempty[sl], ((it / SL) - 1) & 1);
-        const uint32_t xr = smem_u32(xst0 + (size_t)sx * kChunkPart) + tid * 128;
-        const uint32_t lr = smem_u32(lost0 + (size_t)sl * kChunkPart) + tid * 128;
-        uint4 x[8];
-#pragma unroll
-        for (int g = 0; g < 8; ++g)
-          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(x[g].x), "=r"(x[g].y), "=r"(x[g].z), "=r"(x[g].w)
-                       : "r"(xr + ((g ^ sw) << 4)));
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const float4 lo = make_float4(
-              __uint_as_float(x[g].x) - __uint_as_float(x[g].x & 0xFFFFE000u),
-              __uint_as_float(x[g].y) - __uint_as_float(x[g].y & 0xFFFFE000u),
-              __uint_as_float(x[g].z) - __uint_as_float(x[g].z & 0xFFFFE000u),
-              __uint_as_float(x[g].w) - __uint_as_float(x[g].w & 0xFFFFE000u));
-          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lr + ((g ^ sw) << 4)),
-                       "f"(lo.x), "f"(lo.y), "f"(lo.z), "f"(lo.w)
-                       : "memory");
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&lofull[sl]);
-      }
-    }
+  } else if (warp < 4) {  // splitters
+    split_loop(tid, tiles, chunks, SX, SL, xst0, lost0, xfull, lofull, loempty);
   } else if (warp == 4) {  // MMA issuer: waits for W^T in TMEM (named barrier 2)
     asm volatile("bar.sync 2, %0;" ::"r"(32 + kEpi) : "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
