@@ -722,18 +722,39 @@ def auto_band(A: Pcsr, rowptr, colidx, val, K, cfg: Config, features=None, strea
     return Config(V=1, S=0, mode=6), H, info
 
 
+def auto_select(rowptr, colidx, val, K, stream=None):
+    """The library's full selection for a square CSR A and K columns (what
+    bench.py, tools/k_sweep.py and the CLI run): Table-3 features -> decider
+     -> PCSR -> the engine rules of DESIGN.md §5 in order:
+    dense tiles (mode 1), row blocks (mode 5), staged bands (mode 6).
+    One-time preprocessing; returns (cfg, handle to run, info) and the
+    handle serves every later product with this K (or a smaller one)."""
+    n = rowptr.shape[0] - 1
+    nnz = colidx.shape[0]
+    f = pspmm_features_compute(n, nnz, rowptr, colidx, stream=stream)
+    cfg = pspmm_decide_config(f, K)
+    A = pspmm_pcsr_build(n, nnz, rowptr, colidx, val, cfg.V, cfg.S, cfg.omega, cfg.sg_override,
+                         stream)
+    info = {}
+    cfg, info["dense"] = auto_dense(A, rowptr, colidx, val, K, cfg, stream)
+    cfg, A, info["blocks"] = auto_blocks(A, rowptr, colidx, val, K, cfg, stream)
+    cfg, A, info["band"] = auto_band(A, rowptr, colidx, val, K, cfg, f, stream)
+    return cfg, A, info
+
+
 def spmm(rowptr, colidx, val, B, cfg: Config | None = None, stream=None, C=None):
     """The three-phase workflow in one call: features -> decider ->
-    PCSR -> engine.  Returns (C, cfg, Pcsr) so the handle can be reused."""
+    PCSR -> engine, with the engine rules of auto_select when no cfg is
+    given.  Returns (C, cfg, Pcsr) so the handle can be reused."""
     torch = _torch()
     n = rowptr.shape[0] - 1
     nnz = colidx.shape[0]
     K = B.shape[1]
     if cfg is None:
-        f = pspmm_features_compute(n, nnz, rowptr, colidx, stream=stream)
-        cfg = pspmm_decide_config(f, K)
-    A = pspmm_pcsr_build(n, nnz, rowptr, colidx, val, cfg.V, cfg.S, cfg.omega, cfg.sg_override,
-                         stream)
+        cfg, A, _ = auto_select(rowptr, colidx, val, K, stream)
+    else:
+        A = pspmm_pcsr_build(n, nnz, rowptr, colidx, val, cfg.V, cfg.S, cfg.omega,
+                             cfg.sg_override, stream)
     if C is None:
         C = torch.empty((n, K), dtype=torch.float32, device=B.device)
     A.run(B, C, cfg, stream)

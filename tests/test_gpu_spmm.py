@@ -109,6 +109,37 @@ def test_decided_and_alternative_configs(name, K):
         assert_parity(C, ref, mag, f"{name} K{K} {c}")
 
 
+AUTO_GRAPHS = {
+    "cora": lambda: gen.config_graph("cora"),
+    "roadnet_s": lambda: gen.config_graph("roadnet", 0.02),
+    "proteins_s": lambda: gen.config_graph("proteins", 0.05),
+    "clustered_s": lambda: gen.config_graph("proteins_clustered", 0.05),
+    "reddit_s": lambda: gen.config_graph("reddit", 0.01),
+}
+
+
+@pytest.mark.parametrize("name", sorted(AUTO_GRAPHS))
+@pytest.mark.parametrize("K", [32, 128])
+def test_api_spmm_full_selection(name, K):
+    """api.spmm with no cfg runs the library's full selection (auto_select:
+    decider, then the mode-1 / 5 / 6 rules); whatever engine it picks, the
+    product matches the oracle, and the handle is reusable."""
+    api, torch = _api(), _torch()
+    g = AUTO_GRAPHS[name]()
+    B = gen.dense(g.n, K, 90 + K)
+    ref, mag = oracle.spmm(g.rowptr, g.colidx, g.val, B)
+    rp, ci, vl = dev(g)
+    Bd = torch.from_numpy(B).cuda()
+    C, cfg, A = api.spmm(rp, ci, vl, Bd)
+    torch.cuda.synchronize()
+    assert_parity(C.cpu().numpy(), ref, mag, f"api.spmm {name} K{K} {cfg}")
+    C2 = torch.full_like(C, float("nan"))
+    A.run(Bd, C2, cfg)
+    torch.cuda.synchronize()
+    assert_parity(C2.cpu().numpy(), ref, mag, f"reuse {name} K{K} {cfg}")
+    assert cfg.mode in (0, 1, 2, 3, 5, 6)
+
+
 @pytest.mark.parametrize("V,S", [(1, 0), (1, 1), (2, 0), (2, 1)])
 @pytest.mark.parametrize("K", [32, 64, 96, 128, 256, 512])
 @pytest.mark.parametrize("W", [1, 4, 8])
