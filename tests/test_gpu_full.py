@@ -45,6 +45,9 @@ def test_full_config(name):
     cfg, A, blocks = api.auto_blocks(A, rp, ci, vl, K, cfg)  # engine mode 5 rule, as bench.py
     if name == "proteins":
         assert cfg.mode == 5 and blocks["taken"], blocks
+    cfg, A, band = api.auto_band(A, rp, ci, vl, K, cfg)  # engine mode 6 rule, as bench.py
+    if name == "roadnet":
+        assert cfg.mode == 6 and band["taken"], band
     # SpMM, sampled rows (every row for Cora)
     B = gen.config_B(name, g.n)
     Bd = torch.from_numpy(B).cuda()
