@@ -271,7 +271,11 @@ def cusparse_best(g, rp, ci, vl, Bd, K, steps, flush, stream):
             res[names[alg]] = {"status": st}
             continue
         try:
-            ts = time_steps(lambda: lib.pspmm_cusparse_run(plan, s), steps, 3, flush, stream)
+            # a comparison, not the headline: at most 20 steps per algorithm so a
+            # large --steps keeps the run bounded (CSR_ALG1 takes ~0.1 s per
+            # product on the big graphs)
+            ts = time_steps(lambda: lib.pspmm_cusparse_run(plan, s), min(steps, 20), 3, flush,
+                            stream)
             res[names[alg]] = {"ms": float(np.median(ts)), "min_ms": float(min(ts))}
         finally:
             torch.cuda.synchronize()
