@@ -1,5 +1,6 @@
 """Locate wrong elements of the tensor-core dense product (tile / row /
-chunk pattern) over raw-ring depths and tile counts per CTA."""
+chunk pattern) over X-ring depths, both forms (W in shared memory / W in
+tensor memory) and tile counts per CTA."""
 import os
 import sys
 
@@ -19,7 +20,7 @@ def main():
             W = torch.rand((Ki, Ko), device="cuda") * 2 - 1
             ref = (X.double() @ W.double())
             for raw in ("2", "3", "8"):
-                os.environ["PSPMM_GEMM_RAW"] = raw
+                os.environ["PSPMM_GEMM_XS"] = raw
                 T = torch.full((n, Ko), float("nan"), device="cuda")
                 api.pspmm_dense_gemm(X, W, T)
                 torch.cuda.synchronize()
@@ -27,7 +28,7 @@ def main():
                 bad = torch.nonzero(err > 1e-3)
                 rows = torch.unique(bad[:, 0]) if len(bad) else bad
                 tiles = torch.unique(rows // 128) if len(rows) else rows
-                print(f"Ki={Ki} Ko={Ko} n={n} raw={raw}: bad elems {len(bad)} rows {len(rows)} "
+                print(f"Ki={Ki} Ko={Ko} n={n} xs={raw}: bad elems {len(bad)} rows {len(rows)} "
                       f"tiles {len(tiles)} first tiles {tiles[:8].tolist()} "
                       f"rows%128 {sorted(set((rows % 128).tolist()))[:12]} "
                       f"nan {int(torch.isnan(T).sum())}", flush=True)
