@@ -226,6 +226,7 @@ struct GemmArgs {
   int32_t x_stages;   // X ring depth (16 KB each)
   int32_t lo_stages;  // lo ring depth (16 KB each)
   int32_t out_bufs;   // staged output tiles for the TMA-store epilogue (0..2)
+  int32_t fuse;       // 1: Xhi.[Whi | Wlo] as one N = 2 Ko MMA (2 Ko <= 256)
 };
 
 // The kernel (file header): the X chunks (the hi operand) and the lo chunks
@@ -306,9 +307,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float h[4] = {hi.x, hi.y, hi.z, hi.w}, l[4] = {lo.x, lo.y, lo.z, lo.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const uint32_t off = ((uint32_t)(k >> 2) * Ko + 4 * n4 + e) * 16 + (k & 3) * 4;
-            *reinterpret_cast<float *>(wimg + off) = h[e];
-            *reinterpret_cast<float *>(wimg + wpart + off) = l[e];
+            if (a.fuse) {  // one [Ki/4][2 Ko][4] image: hi at n, lo at Ko + n
+              const uint32_t off = ((uint32_t)(k >> 2) * 2 * Ko + 4 * n4 + e) * 16 + (k & 3) * 4;
+              *reinterpret_cast<float *>(wimg + off) = h[e];
+              *reinterpret_cast<float *>(wimg + off + (uint32_t)Ko * 16) = l[e];
+            } else {
+              const uint32_t off = ((uint32_t)(k >> 2) * Ko + 4 * n4 + e) * 16 + (k & 3) * 4;
+              *reinterpret_cast<float *>(wimg + off) = h[e];
+              *reinterpret_cast<float *>(wimg + wpart + off) = l[e];
+            }
           }
         }
       }
@@ -321,15 +328,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       split_loop(tid, tiles, chunks, SX, SL, xst0, lost0, xfull, lofull, loempty);
     } else if (warp == 4) {  // MMA issuer
       if (lane == 0) {
-        const uint32_t id = idesc(Ko);
-        const uint32_t bytes_b = (uint32_t)Ko * 16;
+        const uint32_t id = idesc(Ko), id2 = idesc(2 * Ko);
+        const uint32_t bytes_b = (uint32_t)Ko * 16 * (a.fuse ? 2 : 1);
         const uint32_t whi = smem_u32(wimg), wlo = whi + wpart;
         int it = 0, tl = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
           const int b = tl & 1;
           if (tl >= 2) mbar_wait(&acce[b], ((tl >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t acc = tmem + (uint32_t)(b * Ko);
+          const uint32_t acc = tmem + (uint32_t)(b * Ko * (a.fuse ? 2 : 1));
           for (int c = 0; c < chunks; ++c, ++it) {
             const int sx = it % SX, sl = it % SL;
             mbar_wait(&lofull[sl], (it / SL) & 1);  // the splitters saw xfull: X landed too
@@ -340,10 +347,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ks = 0; ks < kKc / 8; ++ks) {
               const uint64_t dah = desc_sw128(xhi + ks * 32), dal = desc_sw128(xlo + ks * 32);
               const uint32_t ob = (uint32_t)(c * (kKc / 4) + 2 * ks) * bytes_b;
-              const uint64_t dbh = desc(whi + ob, bytes_b, 128), dbl = desc(wlo + ob, bytes_b, 128);
-              mma_tf32(acc, dah, dbh, id, (c > 0 || ks > 0) ? 1u : 0u);
-              mma_tf32(acc, dah, dbl, id, 1u);
-              mma_tf32(acc, dal, dbh, id, 1u);
+              if (a.fuse) {
+                // N = 2 Ko: D[:, 0:Ko] = Xhi.Whi, D[:, Ko:2Ko] = Xhi.Wlo in one
+                // MMA (X_hi read once); then D[:, 0:Ko] += Xlo.Whi (N = Ko)
+                const uint64_t dbw = desc(whi + ob, bytes_b, 128);
+                mma_tf32(acc, dah, dbw, id2, (c > 0 || ks > 0) ? 1u : 0u);
+                mma_tf32(acc, dal, dbw, id, 1u);
+              } else {
+                const uint64_t dbh = desc(whi + ob, bytes_b, 128), dbl = desc(wlo + ob, bytes_b, 128);
+                mma_tf32(acc, dah, dbh, id, (c > 0 || ks > 0) ? 1u : 0u);
+                mma_tf32(acc, dah, dbl, id, 1u);
+                mma_tf32(acc, dal, dbh, id, 1u);
+              }
             }
             mma_commit(&xempty[sx]);
             mma_commit(&loempty[sl]);
@@ -362,7 +377,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int rloc = quarter * 32 + lane;
         const int64_t row = t * kM + rloc;
-        const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * Ko);
+        const uint32_t tb =
+            tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * Ko * (a.fuse ? 2 : 1));
         if (OB > 0) {
           uint8_t *ot = otile + (size_t)(OB == 2 ? (tl & 1) : 0) * kM * Ko * 4;
           if (leader) {
@@ -372,13 +388,26 @@ __global__ void __launch_bounds__(kThreads, 1)
               asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           }
           asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
-          for (int c0 = 0; c0 < Ko; c0 += 64) {
+          const int step = a.fuse ? 32 : 64;  // fused: the Xhi.Wlo half loads beside
+          for (int c0 = 0; c0 < Ko; c0 += step) {
             uint32_t v[4][16];
-            const int nc = Ko - c0 < 64 ? (Ko - c0) / 16 : 4;
+            const int nc = Ko - c0 < step ? (Ko - c0) / 16 : step / 16;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               if (u < nc) tmem_ld16_nowait(tb + c0 + 16 * u, v[u]);
+            if (a.fuse) {
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+                if (u < nc) tmem_ld16_nowait(tb + Ko + c0 + 16 * u, v[2 + u]);
+            }
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (a.fuse) {
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  v[u][j] = __float_as_uint(__uint_as_float(v[u][j]) + __uint_as_float(v[2 + u][j]));
+            }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               if (u < nc) {
@@ -413,6 +442,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < Ko; c += 16) {
           float v[16];
           tmem_ld16(tb + c, v);
+          if (a.fuse) {
+            float w[16];
+            tmem_ld16(tb + Ko + c, w);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] += w[j];
+          }
           if (row < a.n) {
             float4 *dst = reinterpret_cast<float4 *>(a.T + row * a.ldt + c);
 #pragma unroll
@@ -780,6 +815,7 @@ pspmm_status gemm_tc_one(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, in
     args.lo_stages = sl;
     args.out_bufs = ob;
     args.tmem_cols = 512;
+    args.fuse = 0;
     const size_t smem = (size_t)(kSmemSlack + (int64_t)ob * otile + (int64_t)(sx + sl) * kChunkPart);
     PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_wt_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -811,7 +847,10 @@ pspmm_status gemm_tc_one(int64_t n, int32_t Ki, int32_t Ko, const float *d_X, in
   args.x_stages = sx;
   args.lo_stages = sl;
   args.out_bufs = ob;
-  args.tmem_cols = tmem_cols_for(Ko);
+  // the fused-N MMA (X_hi read once per K step): PSPMM_GEMM_FUSE=0 (A/B knob) off
+  const char *fe = std::getenv("PSPMM_GEMM_FUSE");
+  args.fuse = (2 * Ko <= 256 && !(fe && fe[0] == '0')) ? 1 : 0;
+  args.tmem_cols = tmem_cols_for(Ko * (args.fuse ? 2 : 1));
   const size_t smem = (size_t)(kSmemSlack + w + (int64_t)ob * otile + (int64_t)(sx + sl) * kChunkPart);
   PSPMM_CUDA_TRY(cudaFuncSetAttribute(gemm_tc_ring_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -66,7 +66,8 @@ def test_dense_gemm_tensor_core_shapes(n, Ki, Ko, pad, force_cc, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{}, {"PSPMM_GEMM_OB": "2"}, {"PSPMM_GEMM_OB": "0"},
-                                 {"PSPMM_GEMM_WT": "0"}, {"PSPMM_GEMM_WT128": "0"}])
+                                 {"PSPMM_GEMM_WT": "0"}, {"PSPMM_GEMM_WT128": "0"},
+                                 {"PSPMM_GEMM_FUSE": "0"}, {"PSPMM_GEMM_FUSE": "0", "PSPMM_GEMM_OB": "0"}])
 @pytest.mark.parametrize("n,Ki,Ko,pad", [(1, 32, 128, 0), (127, 96, 128, 4), (5000, 64, 128, 0),
                                          (300, 128, 128, 8), (2049, 64, 256, 0),
                                          (1000, 128, 256, 4), (1, 32, 64, 0), (2049, 64, 64, 0),
@@ -77,7 +78,8 @@ def test_dense_gemm_w_in_tmem(n, Ki, Ko, pad, env, monkeypatch):
     output tiles, against the shared-memory form (PSPMM_GEMM_WT=0), and
     Ko = 256 as 128-column blocks (default) or one shared-memory launch
     (PSPMM_GEMM_WT128=0); ragged tiles and padded ld.  The Ko = 64 shapes
-    take the shared-memory form under every setting."""
+    take the shared-memory form, with the fused N = 2 Ko MMA or without it
+    (PSPMM_GEMM_FUSE=0)."""
     import torch
     from paper_2605_15695_b200 import api
     for k, v in env.items():

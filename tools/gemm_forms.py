@@ -19,6 +19,7 @@ sys.path.insert(0, ROOT)
 VARIANTS = [
     ("default", {}),
     ("ring", {"PSPMM_GEMM_WT": "0"}),
+    ("nofuse", {"PSPMM_GEMM_FUSE": "0"}),
     ("no_wt128", {"PSPMM_GEMM_WT128": "0"}),
     ("ob2", {"PSPMM_GEMM_OB": "2"}),
     ("ring_lo3", {"PSPMM_GEMM_LO": "3"}),
@@ -26,7 +27,8 @@ VARIANTS = [
     ("ring_ob1", {"PSPMM_GEMM_OB": "1"}),
     ("ring_ob0", {"PSPMM_GEMM_OB": "0"}),
 ]
-KNOBS = ("PSPMM_GEMM_LO", "PSPMM_GEMM_XS", "PSPMM_GEMM_OB", "PSPMM_GEMM_WT", "PSPMM_GEMM_WT128")
+KNOBS = ("PSPMM_GEMM_LO", "PSPMM_GEMM_XS", "PSPMM_GEMM_OB", "PSPMM_GEMM_WT", "PSPMM_GEMM_WT128",
+         "PSPMM_GEMM_FUSE")
 
 
 def main():
