@@ -21,9 +21,11 @@
 //  - warps 0-3 (splitters): thread r owns row r of the chunk and writes
 //    lo = x - trunc(x) (exact in fp32) into a buffer of the lo ring, in the
 //    same swizzled layout, then fence.proxy.async and an mbarrier arrive;
-//  - warp 4 lane 0 (MMA): per chunk 4 K-steps x 3 tcgen05.mma.kind::tf32
-//    (M = 128, N = Ko, K = 8: Xhi.Whi + Xhi.Wlo + Xlo.Whi) into one of two
-//    TMEM accumulators (2 x Ko columns); tcgen05.commit frees the X stage and
+//  - warp 4 lane 0 (MMA): per chunk 4 K-steps of tcgen05.mma.kind::tf32
+//    (M = 128, K = 8) into one of two TMEM accumulators: Xhi.[Whi | Wlo] as
+//    one N = 2 Ko MMA plus Xlo.Whi (N = Ko) into its first half when
+//    2 Ko <= 256 (the epilogue adds the halves), else three N = Ko MMAs
+//    (Xhi.Whi + Xhi.Wlo + Xlo.Whi); tcgen05.commit frees the X stage and
 //    the lo buffer, and publishes the accumulator;
 //  - warps 5-8 (epilogue): tcgen05.ld 32x32b (warp w reads TMEM lanes
 //    32 (w % 4) .. + 31 = rows of the tile), the tile written into a
